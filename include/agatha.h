@@ -1,0 +1,140 @@
+/*
+ * agatha.h — C ABI of the B200-native guided extension aligner (libagatha.so).
+ *
+ * The operation (§2.1):
+ *   for every (reference window R, read Q) pair of a batch, fill the banded affine-gap
+ *   DP table of Eq. 1-3 anti-diagonal by anti-diagonal
+ *   (l.229), restricted to the k-band (l.248-250), stop at the first anti-diagonal c
+ *   where the Z-drop condition Eq. 4 holds between the global max Eq. 6 and the local
+ *   max Eq. 5 (l.258-266), and report the global max score and its position.
+ * Every reading of a point the paper leaves open (boundary values, tie rules, gating,
+ * N scoring, ...) is listed in DESIGN.md "Readings of the paper" and followed exactly.
+ *
+ * Calling conventions
+ *   - Every function returns 0 (AGATHA_OK) or a negative AGATHA_E* code; the text of a
+ *     code is agatha_strerror(code).  On error the contents of `out` are unspecified.
+ *   - The caller owns every input and output buffer.  A context owns its device scratch
+ *     (packed sequences, plan arrays, queue counter), grows it on demand and frees it in
+ *     agatha_ctx_destroy.  Nothing is retained after a call returns.
+ *   - One context per host thread.  Work is issued on `cuda_stream` (a cudaStream_t, or
+ *     NULL for the legacy default stream); the call returns after the work completes
+ *     (it synchronises `cuda_stream` to collect the error flags).
+ *   - No CPU fallback exists: without a usable sm_100a device every call that needs the
+ *     GPU returns AGATHA_ECUDA.
+ */
+#ifndef AGATHA_H_
+#define AGATHA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ---------------------------------------------------------------- */
+#define AGATHA_OK 0
+#define AGATHA_EINVAL (-1) /* invalid scoring parameters or arguments  */
+#define AGATHA_EEMPTY (-2) /* a sequence of length 0 or n_pairs == 0 */
+#define AGATHA_ECHAR (-3)  /* a non-ACGTN byte under AGATHA_N_REJECT         */
+#define AGATHA_ERANGE (-4) /* band wider than 1024 diagonals, penalties > 127, or a pair so
+                              long that |H| could reach 2^20         */
+#define AGATHA_ECUDA (-5)  /* CUDA runtime failure / no sm_100a device                    */
+#define AGATHA_ENOMEM (-6) /* device allocation failed                                    */
+
+/* ---- batch flags ---------------------------------------------------------------- */
+#define AGATHA_MEM_HOST 0u        /* ref/qry/offsets are host pointers (default)          */
+#define AGATHA_MEM_DEVICE 1u      /* ref/qry/offsets are device pointers                  */
+#define AGATHA_OUT_DEVICE 2u      /* `out` is a device pointer                            */
+#define AGATHA_N_REJECT 0u        /* non-ACGTN bytes are an error (default)               */
+#define AGATHA_N_MAP 4u           /* non-ACGTN bytes are scored as N                      */
+#define AGATHA_PACK_REVERSE 8u    /* agatha_pack4 only: pack back to front                */
+#define AGATHA_ORDER_INPUT 16u    /* dispatch pairs in input order instead of longest-first
+                                     (ordering ablation; results are identical)           */
+
+/* Scoring (Eq. 1-4 symbols).  Penalties are POSITIVE numbers. */
+typedef struct {
+  int32_t match;      /* a, 1..127: S = +a when R[i] == Q[j] and neither is N          */
+  int32_t mismatch;   /* b, 1..127: S = -b                                              */
+  int32_t ambig;      /* n, 0..127: S = -n when either base is N (N vs N included)      */
+  int32_t gap_open;   /* alpha >= beta: a gap run of length k costs alpha + (k-1)*beta  */
+  int32_t gap_extend; /* beta >= 0; also Eq. 4's beta                                   */
+  int32_t band_left;  /* cells with -band_left <= i - j are computed; < 0 = unbounded   */
+  int32_t band_right; /* cells with i - j <= band_right are computed; < 0 = unbounded   */
+  int32_t zdrop;      /* Z >= 0; < 0 disables the Z-drop test                           */
+} agatha_params_t;
+
+/* A batch of n_pairs independent pairs.  Pair k is R = ref[ref_off[k] .. ref_off[k+1])
+ * and Q = qry[qry_off[k] .. qry_off[k+1]), ASCII A/C/G/T/N (either case).  The offset
+ * arrays hold n_pairs + 1 entries and are non-decreasing. */
+typedef struct {
+  const uint8_t* ref;
+  const uint8_t* qry;
+  const uint64_t* ref_off;
+  const uint64_t* qry_off;
+  uint64_t n_pairs;
+  uint32_t flags; /* AGATHA_MEM_* | AGATHA_OUT_DEVICE | AGATHA_N_* | AGATHA_ORDER_INPUT */
+} agatha_batch_t;
+
+/* Per-pair result: 24 bytes, written in pair order. */
+typedef struct {
+  int32_t score;          /* H(i',j'): the global max over computed cells (Eq. 6)       */
+  int32_t ref_end;        /* i' (1-based; ties: earliest anti-diagonal, then smallest i) */
+  int32_t query_end;      /* j' (1-based)                                               */
+  int32_t zdrop_antidiag; /* c = i + j at which Eq. 4 fired; -1 if it never fired       */
+  int64_t cells;          /* in-band in-table cells on anti-diagonals 2 .. c_end        */
+} agatha_result_t;
+
+typedef struct agatha_ctx agatha_ctx_t;
+
+/* Timings and counters of the last agatha_align_batch on this context. */
+typedef struct {
+  float h2d_ms;        /* host->device copy of inputs (0 for device inputs)             */
+  float prep_ms;       /* validation + nominal work (a2) + packing (a1) + LPT sort (a2) */
+  float align_ms;      /* the wavefront align kernel (a3-a8)                             */
+  float d2h_ms;        /* device->host copy of results (0 for device outputs)          */
+  int32_t slots_per_lane; /* K: band diagonals held per lane                             */
+  int32_t grid_blocks; /* persistent grid of the align kernel                            */
+  int32_t kernel_launches; /* kernels of this library launched by the call              */
+  int32_t library_launches; /* CUB radix-sort kernels launched by the call             */
+} agatha_stats_t;
+
+/* Create a context on CUDA device `cuda_device`.  Fails with AGATHA_ECUDA when the
+ * device is not an sm_100 part. */
+int agatha_ctx_create(agatha_ctx_t** ctx, int cuda_device);
+void agatha_ctx_destroy(agatha_ctx_t* ctx);
+
+/* Align every pair of `batch` with `params`; write n_pairs results to `out` (host or
+ * device memory per AGATHA_OUT_DEVICE).  Steps a1-a8 of DESIGN.md all run on the GPU. */
+int agatha_align_batch(agatha_ctx_t* ctx, const agatha_batch_t* batch,
+                       const agatha_params_t* params, agatha_result_t* out, void* cuda_stream);
+
+/* Pack `len` ASCII bases (device memory) into 4-bit codes A0 C1 G2 T3 N4, 8 per uint32
+ * word, earliest base in the low nibble (§2.2 l.279-285),
+ * unused trailing nibbles zero.  `words` (device) receives ceil(len/8) words.  flags:
+ * AGATHA_PACK_REVERSE packs back to front; AGATHA_N_MAP maps invalid bytes to N,
+ * otherwise they yield AGATHA_ECHAR. */
+int agatha_pack4(agatha_ctx_t* ctx, const uint8_t* ascii, uint64_t len, uint32_t* words,
+                 uint32_t flags, void* cuda_stream);
+
+/* The dispatch plan of step a2 for `batch` (device inputs and outputs): nominal[k] =
+ * in-band in-table cell count of pair k (un-terminated), order = pair ids sorted by
+ * descending nominal (ties in any order). */
+int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* batch, const agatha_params_t* params,
+                uint32_t* order, uint32_t* nominal, void* cuda_stream);
+
+/* Debug: per-anti-diagonal local maxima (Eq. 5) of pair `pair` of the last batch run on
+ * this context, as computed by the kernel: for c in [0, cap) score[c] = H*, ref_i[c] =
+ * i* (or -1 when the anti-diagonal is empty or was never reached).  Host outputs.
+ * Requires the pair to be re-run: the call re-aligns `batch` with tracing on. */
+int agatha_localmax_trace(agatha_ctx_t* ctx, const agatha_batch_t* batch,
+                          const agatha_params_t* params, uint64_t pair, int32_t* score,
+                          int32_t* ref_i, int64_t cap, void* cuda_stream);
+
+int agatha_get_stats(const agatha_ctx_t* ctx, agatha_stats_t* stats);
+const char* agatha_strerror(int code);
+int agatha_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AGATHA_H_ */

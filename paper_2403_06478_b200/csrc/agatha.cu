@@ -1,0 +1,852 @@
+// libagatha — B200-native (sm_100a) guided extension alignment behind the C ABI of
+// include/agatha.h.
+//
+// The path:
+//   a1 pack      ASCII -> 4-bit codes (§2.2 l.279-285), R forward, Q reversed
+//   a2 plan      nominal in-band cells per pair, longest-first order (cf. §4.4 l.532-555)
+//   a3 init      boundary row/column values (reading R2)
+//   a4 sweep     Eq. 1-3 (l.207-221) over anti-diagonals (l.229), k-band (l.248-250)
+//   a5 localmax  Eq. 5 (l.264) per anti-diagonal, ties -> smallest i
+//   a6 zdrop     Eq. 4 & 6 (l.258-266), checked every anti-diagonal, early exit
+//   a7 dispatch  persistent warps pulling pairs from a global queue in plan order
+//   a8 result    24-byte record per pair
+//
+// Kernel design: one warp per pair.  The band's D = bl+br+1
+// diagonals are split into 32 lanes x K consecutive diagonals ("slots"); a slot keeps
+// the H / H-alpha / E / F of its diagonal in registers and walks along it, so the whole
+// band front is register-resident.  Anti-diagonal c updates the slots whose diagonal
+// has the parity of c (cells of one anti-diagonal are independent);
+// the only cross-lane dependency per step is one neighbour slot, exchanged with two
+// shuffles.  The local max of every anti-diagonal is one warp REDUX of a packed
+// (score, rank) key; the Z-drop test consumes it one step later so the reduction
+// latency hides behind the next anti-diagonal's cells.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "agatha.h"
+
+namespace {
+
+constexpr int kNegE = -(1 << 22);       // "-infinity" for E/F (and H-alpha) outside the band
+constexpr int kHLimit = 1 << 20;        // every computed in-band H satisfies |H| < kHLimit
+constexpr int kCapStep = 1 << 21;       // per-slot step of the padding cap (see cap_top)
+constexpr int kPadH = -(1 << 21);       // initial H of a padding slot
+constexpr int kNegKey = -(1 << 30);     // key of a cell outside the table
+constexpr int kEmptyH = -kHLimit;       // lane max H at or below this: no cell on the diagonal
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxSlots = 1024;         // 32 lanes x 32 slots
+
+struct AlignArgs {
+  const uint32_t* rw;        // packed R words, pair p starts at word (ref_off[p] >> 3) + p
+  const uint32_t* qw;        // packed reversed-Q words, same addressing with qry_off
+  const uint64_t* roff;
+  const uint64_t* qoff;
+  const uint32_t* order;     // dispatch order (a2)
+  const uint8_t* bad;        // per-pair validation flag from the prep kernel
+  agatha_result_t* out;
+  int* queue;                // global work counter (a7)
+  uint32_t n_pairs;
+  int bl, br;                // band; negative = unbounded
+  int alpha, beta, zdrop;
+  uint32_t T0, T1;           // PRMT score table: byte x = S for code-combination x (0..7)
+  long long trace_pair;      // -1: no tracing
+  int* trace_score;
+  int* trace_i;
+  long long trace_cap;
+};
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// Code combination of eight cells at once (4-bit codes A0 C1 G2 T3 N4 in both R and
+// reversed Q): x = (r ^ q) | (r & q & 4) per nibble.  x == 0 exactly on a match of two
+// non-N bases, x in 1..3 on a mismatch of two non-N bases, x in 4..7 when either is N
+// (N vs N gives 4).  One LOP3.
+__device__ __forceinline__ uint32_t combine(uint32_t r, uint32_t q) {
+  return (r ^ q) | (r & q & 0x44444444u);
+}
+
+__device__ __forceinline__ uint32_t load_word(const uint32_t* base, int w, int nw) {
+  w = w < 0 ? 0 : (w >= nw ? nw - 1 : w);
+  return __ldg(base + w);
+}
+
+// Packed (score, rank) key for the local max (Eq. 5): max key = max H, and among equal
+// H the smallest t (smallest diagonal inside a lane = smallest i on the anti-diagonal).
+__device__ __forceinline__ int make_key(int h, int t) { return h * 16 + (15 - t); }
+
+struct TrueT { static constexpr bool value = true; };
+struct FalseT { static constexpr bool value = false; };
+
+struct PairState {
+  int m, n, dlo, D;
+  int G_H, G_i, G_j, G_d;
+  bool haveG;
+  int term;
+};
+
+// Eq. 4 / Eq. 6 bookkeeping for anti-diagonal c (whose cells had slot parity PARP),
+// given the lane-local key maximum `lk` and the warp max H `rH`.  Returns true when
+// Eq. 4 fires at c (the caller stops).
+template <int K, int PARP, bool TRACE>
+__device__ __forceinline__ bool process_antidiag(PairState& s, const AlignArgs& A, int c, int lk,
+                                                 int rH, int lane, long long pid) {
+  if (rH <= kEmptyH) return false;  // empty anti-diagonal: skipped (reading R11)
+  const bool upd = !s.haveG || rH > s.G_H;
+  const bool chk = s.haveG && A.zdrop >= 0 && (s.G_H - rH > A.zdrop) && (c < s.m + s.n);
+  if (!(upd || chk || TRACE)) return false;
+  // argmax: smallest lane holding rH, then its smallest slot (encoded in the key)
+  const unsigned bal = __ballot_sync(kFull, (lk >> 4) == rH);
+  const int ls = __ffs(bal) - 1;
+  const int kk = __shfl_sync(kFull, lk, ls);
+  const int t = 15 - (kk & 15);
+  const int d = s.dlo + ls * K + PARP + 2 * t;
+  const int i = (c + d) >> 1;
+  const int j = c - i;
+  if (TRACE && pid == A.trace_pair && lane == 0 && c < A.trace_cap) {
+    A.trace_score[c] = rH;
+    A.trace_i[c] = i;
+  }
+  if (chk && s.G_i < i && s.G_j < j) {
+    const int gap = d - s.G_d;
+    if (s.G_H - rH > A.zdrop + A.beta * (gap < 0 ? -gap : gap)) {
+      s.term = c;
+      return true;
+    }
+  }
+  if (upd) {
+    s.G_H = rH;
+    s.G_i = i;
+    s.G_j = j;
+    s.G_d = d;
+    s.haveG = true;
+  }
+  return false;
+}
+
+// One anti-diagonal step: update the K/2 slots of parity PAR.  `S` holds the
+// substitution scores of the step as sign-extendable bytes (4 cells per word).
+//
+// Storage per slot: H, and E and F shifted by +alpha (Eh = E + alpha, Fh = F + alpha),
+// which turns Eq. 2-3 into one VIADDMNMX each without a stored H - alpha:
+//   Eh(i,j) = max(Eh(i-1,j) - beta, H(i-1,j))      [= Eq. 2 + alpha]
+//   Fh(i,j) = max(Fh(i,j-1) - beta, H(i,j-1))      [= Eq. 3 + alpha]
+//   H(i,j)  = max(max(Eh, Fh) - alpha, H(i-1,j-1) + S)   [= Eq. 1]
+template <int K, int PAR, bool MASKED>
+__device__ __forceinline__ int step_cells(int (&H)[K], int (&Eh)[K], int (&Fh)[K],
+                                          const uint32_t (&S)[K / 8], int lane, int nalpha,
+                                          int nbeta, int capT, int tlo, int thi) {
+  // edge exchange: the one neighbour slot that lives in the adjacent lane
+  int xH, xEF;
+  if (PAR == 0) {
+    xH = __shfl_up_sync(kFull, H[K - 1], 1);
+    xEF = __shfl_up_sync(kFull, Eh[K - 1], 1);
+    if (lane == 0) { xH = kNegE; xEF = kNegE; }   // below the band: -infinity
+  } else {
+    xH = __shfl_down_sync(kFull, H[0], 1);
+    xEF = __shfl_down_sync(kFull, Fh[0], 1);
+    if (lane == 31) { xH = kNegE; xEF = kNegE; }  // above the last lane: -infinity
+  }
+  int lk = kNegKey, kprev = kNegKey;
+#pragma unroll
+  for (int t = 0; t < K / 2; ++t) {
+    const int k = PAR + 2 * t;
+    const int hu = (k == 0) ? xH : H[k - 1];
+    const int eu = (k == 0) ? xEF : Eh[k - 1];
+    const int hl = (k == K - 1) ? xH : H[k + 1];
+    const int fl = (k == K - 1) ? xEF : Fh[k + 1];
+    const int e = __viaddmax_s32(eu, nbeta, hu);           // Eq. 2 (+alpha)
+    const int f = __viaddmax_s32(fl, nbeta, hl);           // Eq. 3 (+alpha)
+    const uint32_t sel = (uint32_t)(t & 3) | ((uint32_t)((t & 3) | 8) * 0x1110u);
+    const int sub = (int)prmt(S[t >> 2], 0u, sel);         // S(R[i],Q[j]), sign-extended
+    int h = __viaddmax_s32(max(e, f), nalpha, H[k] + sub); // Eq. 1
+    h = __viaddmin_s32(capT, -k * kCapStep, h);            // padding slots stay below -2^20
+    int key = make_key(h, t);
+    if (MASKED) {
+      const bool v = (t >= tlo) && (t <= thi);
+      H[k] = v ? h : H[k];
+      Eh[k] = v ? e : kNegE;
+      Fh[k] = v ? f : kNegE;
+      key = v ? key : kNegKey;
+    } else {
+      H[k] = h;
+      Eh[k] = e;
+      Fh[k] = f;
+    }
+    if (t & 1) lk = __vimax3_s32(lk, kprev, key); else kprev = key;  // Eq. 5, 2 cells per VIMNMX3
+  }
+  return (K / 2) & 1 ? max(lk, kprev) : lk;
+}
+
+template <int K, bool TRACE>
+__device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
+  const uint64_t r0 = A.roff[pid], q0 = A.qoff[pid];
+  const int m = (int)(A.roff[pid + 1] - r0);
+  const int n = (int)(A.qoff[pid + 1] - q0);
+  if (A.bad[pid]) {
+    if (lane == 0) {
+      agatha_result_t z = {0, 0, 0, -1, 0};
+      A.out[pid] = z;
+    }
+    return;
+  }
+  const uint32_t* Rw = A.rw + (r0 >> 3) + pid;
+  const uint32_t* Qw = A.qw + (q0 >> 3) + pid;
+  const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
+  const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;   // diagonals beyond hold no cell
+  const int br = (A.br < 0 || A.br > m) ? m : A.br;
+  const int alpha = A.alpha, beta = A.beta, nbeta = -A.beta, nalpha = -A.alpha;
+
+  PairState s;
+  s.m = m; s.n = n; s.dlo = -bl; s.D = bl + br + 1;
+  s.haveG = false; s.G_H = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.term = -1;
+  const int dlo = -bl, D = s.D;
+
+  // padding cap: slot k of this lane is capped at capT - k*kCapStep
+  const int gbase = lane * K;
+  int capT;
+  if (gbase + K <= D) capT = 1 << 30;
+  else if (gbase >= D) capT = -kHLimit;
+  else capT = (D - gbase - 1) * kCapStep + kHLimit;
+
+  // a3: boundary values H(d,0) / H(0,-d) (reading R2); E = F = -infinity
+  int H[K], Eh[K], Fh[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int g = gbase + k, d = dlo + g;
+    const int ad = d < 0 ? -d : d;
+    H[k] = (g < D) ? (d == 0 ? 0 : -(alpha + (ad - 1) * beta)) : kPadH;
+    Eh[k] = kNegE;
+    Fh[k] = kNegE;
+  }
+
+  // phases: head (masked) / steady (every band slot in the table) / tail (masked)
+  auto fdiag = [&](int d) { return 2 * min(m, n + d) - d; };  // last anti-diagonal of diagonal d
+  const int dhi = br;
+  const int cs = 2 + max(bl, br);
+  const int ce = min(fdiag(dlo), fdiag(dhi));
+  const int dmid = min(max(m - n, dlo), dhi);
+  const int c_last = fdiag(dmid);
+
+  // sequence windows (R forward, Q reversed), nibble-granular, uniform phase across lanes
+  int cb = 2 - (dlo & 1);                     // first step parity 0: cb == dlo (mod 2)
+  int u = (cb + dlo) >> 1;
+  int rpos = u - 1 + lane * (K / 2);          // nibble index of R[i] at t = 0, PAR = 0
+  int wR = rpos >> 3, oR = rpos & 7;
+  uint32_t Wr0 = load_word(Rw, wR, nwR), Wr1 = load_word(Rw, wR + 1, nwR),
+           Wr2 = load_word(Rw, wR + 2, nwR), nR = load_word(Rw, wR + 3, nwR);
+  int qpos = n + dlo - u + lane * (K / 2);    // nibble index of Qrev[x] at t = 0
+  int wQ = qpos >> 3, oQ = qpos & 7;
+  uint32_t Wq0 = load_word(Qw, wQ, nwQ), Wq1 = load_word(Qw, wQ + 1, nwQ),
+           Wq2 = load_word(Qw, wQ + 2, nwQ), nQ = load_word(Qw, wQ - 1, nwQ);
+
+  const uint32_t T0 = A.T0, T1 = A.T1;
+  int lk_prev = kNegKey, rH_prev = kEmptyH - 1;  // nothing pending before the first step
+  bool stop = false;
+
+  auto iteration = [&](auto masked_tag) {
+    constexpr bool MASKED = decltype(masked_tag)::value;
+    constexpr int NG = (K >= 16) ? K / 16 : 1;
+    uint32_t qg[NG], S[K / 8 > 0 ? K / 8 : 1];
+    const uint32_t Wq[3] = {Wq0, Wq1, Wq2}, Wr[3] = {Wr0, Wr1, Wr2};
+#pragma unroll
+    for (int g = 0; g < NG; ++g) qg[g] = __funnelshift_rc(Wq[g], Wq[g + 1], 4 * oQ);
+    // ---- step PAR = 0, anti-diagonal cb ----
+    {
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const uint32_t x = combine(__funnelshift_rc(Wr[g], Wr[g + 1], 4 * oR), qg[g]);
+        S[2 * g] = prmt(T0, T1, x);
+        if (2 * g + 1 < K / 8) S[2 * g + 1] = prmt(T0, T1, x >> 16);
+      }
+      int tlo = 0, thi = K;
+      if (MASKED) {
+        const int ib = u + lane * (K / 2), jb = u - dlo - lane * (K / 2);
+        tlo = max(1 - ib, jb - n);
+        thi = min(m - ib, jb - 1);
+      }
+      const int lk = step_cells<K, 0, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi);
+      const int rH = __reduce_max_sync(kFull, lk >> 4);
+      if (process_antidiag<K, 1, TRACE>(s, A, cb - 1, lk_prev, rH_prev, lane, pid)) { stop = true; return; }
+      lk_prev = lk;
+      rH_prev = rH;
+    }
+    // ---- step PAR = 1, anti-diagonal cb + 1 ----
+    {
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const uint32_t x = combine(__funnelshift_rc(Wr[g], Wr[g + 1], 4 * oR + 4), qg[g]);
+        S[2 * g] = prmt(T0, T1, x);
+        if (2 * g + 1 < K / 8) S[2 * g + 1] = prmt(T0, T1, x >> 16);
+      }
+      int tlo = 0, thi = K;
+      if (MASKED) {
+        const int ib = u + 1 + lane * (K / 2), jb = u - dlo - lane * (K / 2);
+        tlo = max(1 - ib, jb - n);
+        thi = min(m - ib, jb - 1);
+      }
+      const int lk = step_cells<K, 1, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi);
+      const int rH = __reduce_max_sync(kFull, lk >> 4);
+      if (process_antidiag<K, 0, TRACE>(s, A, cb, lk_prev, rH_prev, lane, pid)) { stop = true; return; }
+      lk_prev = lk;
+      rH_prev = rH;
+    }
+    // ---- advance the windows by one base each: R forward, reversed Q backward ----
+    cb += 2;
+    ++u;
+    if (++oR == 8) {
+      oR = 0;
+      ++wR;
+      Wr0 = Wr1; Wr1 = Wr2; Wr2 = nR;
+      nR = load_word(Rw, wR + 3, nwR);
+    }
+    if (--oQ < 0) {
+      oQ = 7;
+      --wQ;
+      Wq2 = Wq1; Wq1 = Wq0; Wq0 = nQ;
+      nQ = load_word(Qw, wQ - 1, nwQ);
+    }
+  };
+
+  while (!stop && cb <= c_last && cb < cs) iteration(TrueT{});
+  while (!stop && cb + 1 <= ce) iteration(FalseT{});
+  while (!stop && cb <= c_last) iteration(TrueT{});
+  if (!stop) {
+    // the last computed step (cb - 1, slot parity 1) is still pending
+    process_antidiag<K, 1, TRACE>(s, A, cb - 1, lk_prev, rH_prev, lane, pid);
+  }
+
+  // a8: cells = in-band in-table cells on anti-diagonals 2 .. c_end (closed form per slot)
+  const int c_end = s.term >= 0 ? s.term : m + n;
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int g = gbase + k;
+    if (g < D) {
+      const int d = dlo + g;
+      const int clo = (d < 0 ? -d : d) + 2;
+      const int hi = min(fdiag(d), c_end);
+      if (hi >= clo) cnt += ((hi - clo) >> 1) + 1;
+    }
+  }
+  cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
+  if (lane == 0) {
+    agatha_result_t r;
+    r.score = s.G_H;
+    r.ref_end = s.G_i;
+    r.query_end = s.G_j;
+    r.zdrop_antidiag = s.term;
+    r.cells = cnt;
+    A.out[pid] = r;
+  }
+}
+
+// Register budget: the band front (H for all K slots, E/F/H-alpha for the last parity)
+// plus the per-pair state needs ~150 registers at K = 32, so 3 blocks of 4 warps
+// (12 warps, 3 per scheduler) per SM; K = 16 fits 4 blocks.
+template <int K>
+struct MinBlocks { static constexpr int value = K >= 32 ? 3 : 4; };
+
+template <int K, bool TRACE>
+__global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignArgs A) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(A.queue, 1);
+    q = __shfl_sync(kFull, q, 0);
+    if ((uint32_t)q >= A.n_pairs) break;
+    align_pair<K, TRACE>(A, A.order[q], lane);
+  }
+}
+
+// ---- a1: pack (one warp per pair; R forward, Q reversed) ---------------------------
+
+__device__ __forceinline__ uint32_t base_code(uint8_t ch, bool nmap, int* err) {
+  const uint8_t u = ch & 0xDF;  // upper case
+  uint32_t c;
+  if (u == 'A') c = 0;
+  else if (u == 'C') c = 1;
+  else if (u == 'G') c = 2;
+  else if (u == 'T') c = 3;
+  else if (u == 'N') c = 4;
+  else {
+    c = 4;
+    if (!nmap) *err = 1;
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint32_t pack_word(const uint8_t* seq, int64_t len, int64_t w, bool rev,
+                                              bool nmap, int* err) {
+  uint32_t word = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int64_t k = 8 * w + t;
+    if (k < len) {
+      const uint8_t ch = rev ? seq[len - 1 - k] : seq[k];
+      word |= base_code(ch, nmap, err) << (4 * t);
+    }
+  }
+  return word;
+}
+
+__global__ void pack_pairs_kernel(const uint8_t* __restrict__ ref, const uint8_t* __restrict__ qry,
+                                  const uint64_t* __restrict__ roff, const uint64_t* __restrict__ qoff,
+                                  uint64_t n_pairs, uint32_t* __restrict__ rw, uint32_t* __restrict__ qw,
+                                  bool nmap, int* __restrict__ err_flags) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  int err = 0;
+  for (uint64_t p = warp; p < n_pairs; p += nwarps) {
+    const uint64_t r0 = roff[p], q0 = qoff[p];
+    const int64_t m = (int64_t)(roff[p + 1] - r0), n = (int64_t)(qoff[p + 1] - q0);
+    uint32_t* R = rw + (r0 >> 3) + p;
+    uint32_t* Q = qw + (q0 >> 3) + p;
+    for (int64_t w = lane; w < (m + 7) / 8; w += 32) R[w] = pack_word(ref + r0, m, w, false, nmap, &err);
+    for (int64_t w = lane; w < (n + 7) / 8; w += 32) Q[w] = pack_word(qry + q0, n, w, true, nmap, &err);
+  }
+  if (__any_sync(kFull, err) && lane == 0) atomicOr(err_flags, 1);
+}
+
+__global__ void pack_seq_kernel(const uint8_t* __restrict__ seq, uint64_t len, uint32_t* __restrict__ words,
+                                bool rev, bool nmap, int* __restrict__ err_flags) {
+  int err = 0;
+  const uint64_t nw = (len + 7) / 8;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw;
+       w += (uint64_t)gridDim.x * blockDim.x)
+    words[w] = pack_word(seq, (int64_t)len, (int64_t)w, rev, nmap, &err);
+  if (err) atomicOr(err_flags, 1);
+}
+
+// ---- a2: validation + nominal work (one warp per pair) ------------------------------
+
+struct PrepArgs {
+  const uint64_t* roff;
+  const uint64_t* qoff;
+  uint64_t n_pairs;
+  int bl, br, alpha, beta, maxs;  // maxs = max(a, b, n)
+  uint32_t* nominal;
+  uint32_t* iota;
+  uint8_t* bad;
+  int* err_flags;   // bit 1: empty sequence, bit 2: out of range
+  int* max_slots;   // max D over the batch
+};
+
+__global__ void prep_kernel(PrepArgs P) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t p = warp; p < P.n_pairs; p += nwarps) {
+    const int64_t m = (int64_t)(P.roff[p + 1] - P.roff[p]);
+    const int64_t n = (int64_t)(P.qoff[p + 1] - P.qoff[p]);
+    int flag = 0;
+    int64_t bl = (P.bl < 0 || P.bl > n) ? n : P.bl;
+    int64_t br = (P.br < 0 || P.br > m) ? m : P.br;
+    if (m <= 0 || n <= 0) flag = 2;
+    const int64_t D = bl + br + 1;
+    // |H| bound: alpha + max(bl,br)*beta + max(a,b,n)*min(m,n)
+    const int64_t hb = (int64_t)P.alpha + (bl > br ? bl : br) * (int64_t)P.beta +
+                       (int64_t)P.maxs * (m < n ? m : n);
+    if (!flag && (D > kMaxSlots || hb >= kHLimit - 16 || m + n >= (1LL << 30))) flag = 4;
+    // nominal in-band in-table cells: sum over diagonals d of |{i : 1<=i<=m, 1<=i-d<=n}|
+    uint64_t cnt = 0;
+    if (!flag) {
+      for (int64_t d = -bl + lane; d <= br; d += 32) {
+        const int64_t lo = d + 1 > 1 ? d + 1 : 1;
+        const int64_t hi = n + d < m ? n + d : m;
+        if (hi >= lo) cnt += (uint64_t)(hi - lo + 1);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+    if (lane == 0) {
+      P.nominal[p] = (uint32_t)(cnt > 0xffffffffull ? 0xffffffffull : cnt);
+      P.iota[p] = (uint32_t)p;
+      P.bad[p] = (uint8_t)(flag != 0);
+      if (flag) atomicOr(P.err_flags, flag);
+      else atomicMax(P.max_slots, (int)D);
+    }
+  }
+}
+
+}  // namespace
+
+// ===================================================================================
+// Host runtime
+// ===================================================================================
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct agatha_ctx {
+  int device = 0;
+  int num_sms = 0;
+  DevBuf ref_ascii, qry_ascii, ref_off, qry_off;     // staging for host inputs
+  DevBuf rw, qw;                                      // packed sequences
+  DevBuf nominal, nominal_sorted, iota, order, bad;   // plan
+  DevBuf sort_tmp;
+  DevBuf results;                                     // staging for host outputs
+  DevBuf scalars;                                     // err_flags, max_slots, queue
+  DevBuf trace;                                       // trace buffers
+  int* h_scalars = nullptr;                           // pinned mirror of scalars
+  cudaEvent_t ev[6];
+  agatha_stats_t stats;
+};
+
+namespace {
+
+int grow(DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return AGATHA_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  size_t want = bytes + bytes / 8;
+  if (cudaMalloc(&b.p, want) != cudaSuccess) {
+    cudaGetLastError();
+    return AGATHA_ENOMEM;
+  }
+  b.cap = want;
+  return AGATHA_OK;
+}
+
+int check_params(const agatha_params_t* p) {
+  if (!p) return AGATHA_EINVAL;
+  if (p->match <= 0 || p->mismatch <= 0 || p->ambig < 0) return AGATHA_EINVAL;
+  if (p->gap_extend < 0 || p->gap_open < p->gap_extend) return AGATHA_EINVAL;
+  if (p->match > 127 || p->mismatch > 127 || p->ambig > 127) return AGATHA_ERANGE;
+  if (p->gap_open > 65535 || p->zdrop > (1 << 24)) return AGATHA_ERANGE;
+  if (p->band_left > 4096 || p->band_right > 4096) return AGATHA_ERANGE;
+  return AGATHA_OK;
+}
+
+// Score table for prmt: byte x (0..7) = S for code combination x (see combine()).
+void score_table(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
+  uint8_t t[8];
+  t[0] = (uint8_t)(int8_t)p->match;
+  for (int x = 1; x < 4; ++x) t[x] = (uint8_t)(int8_t)(-p->mismatch);
+  for (int x = 4; x < 8; ++x) t[x] = (uint8_t)(int8_t)(-p->ambig);
+  *T0 = t[0] | (t[1] << 8) | (t[2] << 16) | ((uint32_t)t[3] << 24);
+  *T1 = t[4] | (t[5] << 8) | (t[6] << 16) | ((uint32_t)t[7] << 24);
+}
+
+#define CUDA_TRY(x)                          \
+  do {                                       \
+    cudaError_t e_ = (x);                    \
+    if (e_ != cudaSuccess) {                 \
+      fprintf(stderr, "libagatha: %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return AGATHA_ECUDA;                   \
+    }                                        \
+  } while (0)
+
+template <int K, bool TRACE>
+int launch_align(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
+  static int occ = -1;
+  if (occ < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align_kernel<K, TRACE>, 128, 0) != cudaSuccess) {
+      cudaGetLastError();
+      occ = 1;
+    }
+    if (occ < 1) occ = 1;
+  }
+  const long long want = (long long)ctx->num_sms * occ;      // persistent: fill every SM once
+  const long long need = ((long long)A.n_pairs + 3) / 4;    // 4 warps (pairs in flight) per block
+  int grid = (int)(want < need ? want : need);
+  if (grid < 1) grid = 1;
+  *grid_out = grid;
+  align_kernel<K, TRACE><<<grid, 128, 0, st>>>(A);
+  CUDA_TRY(cudaGetLastError());
+  return AGATHA_OK;
+}
+
+// Shared body of agatha_align_batch / agatha_localmax_trace.
+int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p,
+              agatha_result_t* out, cudaStream_t st, long long trace_pair, int* trace_score,
+              int* trace_i, long long trace_cap) {
+  if (!ctx || !b || !out) return AGATHA_EINVAL;
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (b->n_pairs == 0) return AGATHA_EEMPTY;
+  if (b->n_pairs >= (1ull << 31)) return AGATHA_ERANGE;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  memset(&ctx->stats, 0, sizeof(ctx->stats));
+  const uint64_t P = b->n_pairs;
+  const bool dev_in = (b->flags & AGATHA_MEM_DEVICE) != 0;
+  const bool dev_out = (b->flags & AGATHA_OUT_DEVICE) != 0;
+  const bool nmap = (b->flags & AGATHA_N_MAP) != 0;
+
+  CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
+  uint64_t tot_r, tot_q;
+  const uint8_t *d_ref, *d_qry;
+  const uint64_t *d_roff, *d_qoff;
+  if (dev_in) {
+    uint64_t tmp[2];
+    CUDA_TRY(cudaMemcpyAsync(&tmp[0], b->ref_off + P, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&tmp[1], b->qry_off + P, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    tot_r = tmp[0];
+    tot_q = tmp[1];
+    d_ref = b->ref; d_qry = b->qry; d_roff = b->ref_off; d_qoff = b->qry_off;
+  } else {
+    tot_r = b->ref_off[P];
+    tot_q = b->qry_off[P];
+    if ((rc = grow(ctx->ref_ascii, tot_r)) || (rc = grow(ctx->qry_ascii, tot_q)) ||
+        (rc = grow(ctx->ref_off, 8 * (P + 1))) || (rc = grow(ctx->qry_off, 8 * (P + 1))))
+      return rc;
+    CUDA_TRY(cudaMemcpyAsync(ctx->ref_ascii.p, b->ref, tot_r, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->qry_ascii.p, b->qry, tot_q, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->ref_off.p, b->ref_off, 8 * (P + 1), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->qry_off.p, b->qry_off, 8 * (P + 1), cudaMemcpyHostToDevice, st));
+    d_ref = (const uint8_t*)ctx->ref_ascii.p;
+    d_qry = (const uint8_t*)ctx->qry_ascii.p;
+    d_roff = (const uint64_t*)ctx->ref_off.p;
+    d_qoff = (const uint64_t*)ctx->qry_off.p;
+  }
+  CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
+
+  // device scratch
+  size_t sort_bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const uint32_t*)nullptr,
+                                            (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                            (uint32_t*)nullptr, (int)P, 0, 32, st);
+  if ((rc = grow(ctx->rw, 4 * (tot_r / 8 + P + 2))) || (rc = grow(ctx->qw, 4 * (tot_q / 8 + P + 2))) ||
+      (rc = grow(ctx->nominal, 4 * P)) || (rc = grow(ctx->nominal_sorted, 4 * P)) ||
+      (rc = grow(ctx->iota, 4 * P)) || (rc = grow(ctx->order, 4 * P)) || (rc = grow(ctx->bad, P)) ||
+      (rc = grow(ctx->sort_tmp, sort_bytes)) || (rc = grow(ctx->scalars, 64)))
+    return rc;
+  agatha_result_t* d_out = out;
+  if (!dev_out) {
+    if ((rc = grow(ctx->results, sizeof(agatha_result_t) * P))) return rc;
+    d_out = (agatha_result_t*)ctx->results.p;
+  }
+  int* d_sc = (int*)ctx->scalars.p;  // [0] err_flags [1] max_slots [2] queue
+  CUDA_TRY(cudaMemsetAsync(d_sc, 0, 16, st));
+
+  const int maxs = p->match > p->mismatch ? (p->match > p->ambig ? p->match : p->ambig)
+                                          : (p->mismatch > p->ambig ? p->mismatch : p->ambig);
+  PrepArgs pa;
+  pa.roff = d_roff; pa.qoff = d_qoff; pa.n_pairs = P;
+  pa.bl = p->band_left; pa.br = p->band_right; pa.alpha = p->gap_open; pa.beta = p->gap_extend;
+  pa.maxs = maxs;
+  pa.nominal = (uint32_t*)ctx->nominal.p; pa.iota = (uint32_t*)ctx->iota.p;
+  pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1;
+  const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
+  prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
+  CUDA_TRY(cudaGetLastError());
+  pack_pairs_kernel<<<prep_blocks, 256, 0, st>>>(d_ref, d_qry, d_roff, d_qoff, P, (uint32_t*)ctx->rw.p,
+                                                 (uint32_t*)ctx->qw.p, nmap, d_sc);
+  CUDA_TRY(cudaGetLastError());
+  int launches = 2, lib_launches = 0;
+  const uint32_t* d_order = (const uint32_t*)ctx->iota.p;
+  if (!(b->flags & AGATHA_ORDER_INPUT)) {
+    size_t tb = ctx->sort_tmp.cap;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(
+        ctx->sort_tmp.p, tb, (const uint32_t*)ctx->nominal.p, (uint32_t*)ctx->nominal_sorted.p,
+        (const uint32_t*)ctx->iota.p, (uint32_t*)ctx->order.p, (int)P, 0, 32, st));
+    d_order = (const uint32_t*)ctx->order.p;
+    lib_launches = 4;
+  }
+  // K (slots per lane) from the widest band in the batch
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const int err0 = ctx->h_scalars[0], maxD = ctx->h_scalars[1];
+  if (err0 & 1) return AGATHA_ECHAR;
+  if (err0 & 2) return AGATHA_EEMPTY;
+  if (err0 & 4) return AGATHA_ERANGE;
+  CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
+
+  AlignArgs A;
+  A.rw = (const uint32_t*)ctx->rw.p; A.qw = (const uint32_t*)ctx->qw.p;
+  A.roff = d_roff; A.qoff = d_qoff; A.order = d_order; A.bad = (const uint8_t*)ctx->bad.p;
+  A.out = d_out; A.queue = d_sc + 2; A.n_pairs = (uint32_t)P;
+  A.bl = p->band_left; A.br = p->band_right;
+  A.alpha = p->gap_open; A.beta = p->gap_extend; A.zdrop = p->zdrop;
+  score_table(p, &A.T0, &A.T1);
+  A.trace_pair = trace_pair; A.trace_score = trace_score; A.trace_i = trace_i; A.trace_cap = trace_cap;
+  int grid = 0;
+  const int K = maxD <= 512 ? 16 : 32;
+  if (trace_pair >= 0) {
+    rc = (K == 16) ? launch_align<16, true>(ctx, A, st, &grid) : launch_align<32, true>(ctx, A, st, &grid);
+  } else {
+    rc = (K == 16) ? launch_align<16, false>(ctx, A, st, &grid) : launch_align<32, false>(ctx, A, st, &grid);
+  }
+  if (rc) return rc;
+  ++launches;
+  CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
+  if (!dev_out)
+    CUDA_TRY(cudaMemcpyAsync(out, d_out, sizeof(agatha_result_t) * P, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(ctx->ev[4], st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  cudaEventElapsedTime(&ctx->stats.h2d_ms, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&ctx->stats.prep_ms, ctx->ev[1], ctx->ev[2]);
+  cudaEventElapsedTime(&ctx->stats.align_ms, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&ctx->stats.d2h_ms, ctx->ev[3], ctx->ev[4]);
+  ctx->stats.slots_per_lane = K;
+  ctx->stats.grid_blocks = grid;
+  ctx->stats.kernel_launches = launches;
+  ctx->stats.library_launches = lib_launches;
+  return AGATHA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int agatha_version(void) { return 1; }
+
+const char* agatha_strerror(int code) {
+  switch (code) {
+    case AGATHA_OK: return "ok";
+    case AGATHA_EINVAL: return "invalid argument or scoring parameters";
+    case AGATHA_EEMPTY: return "empty sequence or empty batch";
+    case AGATHA_ECHAR: return "non-ACGTN byte in a sequence";
+    case AGATHA_ERANGE: return "band, penalty or sequence length beyond the supported range";
+    case AGATHA_ECUDA: return "CUDA error or no sm_100 device";
+    case AGATHA_ENOMEM: return "device allocation failed";
+    default: return "unknown error";
+  }
+}
+
+int agatha_ctx_create(agatha_ctx_t** out, int device) {
+  if (!out) return AGATHA_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return AGATHA_ECUDA;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return AGATHA_ECUDA;
+  if (prop.major != 10) return AGATHA_ECUDA;  // built for sm_100a only
+  if (cudaSetDevice(device) != cudaSuccess) return AGATHA_ECUDA;
+  agatha_ctx* ctx = new agatha_ctx();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  for (int i = 0; i < 6; ++i) cudaEventCreate(&ctx->ev[i]);
+  if (cudaMallocHost(&ctx->h_scalars, 64) != cudaSuccess) {
+    delete ctx;
+    return AGATHA_ENOMEM;
+  }
+  *out = ctx;
+  return AGATHA_OK;
+}
+
+void agatha_ctx_destroy(agatha_ctx_t* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  DevBuf* bufs[] = {&ctx->ref_ascii, &ctx->qry_ascii, &ctx->ref_off, &ctx->qry_off, &ctx->rw,
+                    &ctx->qw, &ctx->nominal, &ctx->nominal_sorted, &ctx->iota, &ctx->order,
+                    &ctx->bad, &ctx->sort_tmp, &ctx->results, &ctx->scalars, &ctx->trace};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  for (int i = 0; i < 6; ++i) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
+  delete ctx;
+}
+
+int agatha_align_batch(agatha_ctx_t* ctx, const agatha_batch_t* batch, const agatha_params_t* params,
+                       agatha_result_t* out, void* stream) {
+  return run_batch(ctx, batch, params, out, (cudaStream_t)stream, -1, nullptr, nullptr, 0);
+}
+
+int agatha_localmax_trace(agatha_ctx_t* ctx, const agatha_batch_t* batch, const agatha_params_t* params,
+                          uint64_t pair, int32_t* score, int32_t* ref_i, int64_t cap, void* stream) {
+  if (!ctx || !batch || !score || !ref_i || cap <= 0 || pair >= batch->n_pairs) return AGATHA_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = grow(ctx->trace, 8 * (size_t)cap + sizeof(agatha_result_t) * batch->n_pairs);
+  if (rc) return rc;
+  int* ts = (int*)ctx->trace.p;
+  int* ti = ts + cap;
+  agatha_result_t* tout = (agatha_result_t*)(ti + cap);
+  CUDA_TRY(cudaMemsetAsync(ts, 0, 4 * (size_t)cap, st));
+  CUDA_TRY(cudaMemsetAsync(ti, 0xff, 4 * (size_t)cap, st));
+  agatha_batch_t b2 = *batch;
+  b2.flags |= AGATHA_OUT_DEVICE;
+  rc = run_batch(ctx, &b2, params, tout, st, (long long)pair, ts, ti, cap);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(score, ts, 4 * (size_t)cap, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ref_i, ti, 4 * (size_t)cap, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return AGATHA_OK;
+}
+
+int agatha_pack4(agatha_ctx_t* ctx, const uint8_t* ascii, uint64_t len, uint32_t* words, uint32_t flags,
+                 void* stream) {
+  if (!ctx || !ascii || !words) return AGATHA_EINVAL;
+  if (len == 0) return AGATHA_EEMPTY;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  int rc = grow(ctx->scalars, 64);
+  if (rc) return rc;
+  int* d_sc = (int*)ctx->scalars.p;
+  CUDA_TRY(cudaMemsetAsync(d_sc, 0, 4, st));
+  const uint64_t nw = (len + 7) / 8;
+  int blocks = (int)((nw + 255) / 256 < 8192 ? (nw + 255) / 256 : 8192);
+  pack_seq_kernel<<<blocks, 256, 0, st>>>(ascii, len, words, (flags & AGATHA_PACK_REVERSE) != 0,
+                                          (flags & AGATHA_N_MAP) != 0, d_sc);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return ctx->h_scalars[0] ? AGATHA_ECHAR : AGATHA_OK;
+}
+
+int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* b, const agatha_params_t* p, uint32_t* order,
+                uint32_t* nominal, void* stream) {
+  if (!ctx || !b || !order || !nominal) return AGATHA_EINVAL;
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (b->n_pairs == 0) return AGATHA_EEMPTY;
+  if (!(b->flags & AGATHA_MEM_DEVICE)) return AGATHA_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  const uint64_t P = b->n_pairs;
+  size_t sort_bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const uint32_t*)nullptr,
+                                            (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                            (uint32_t*)nullptr, (int)P, 0, 32, st);
+  if ((rc = grow(ctx->iota, 4 * P)) || (rc = grow(ctx->bad, P)) || (rc = grow(ctx->sort_tmp, sort_bytes)) ||
+      (rc = grow(ctx->scalars, 64)))
+    return rc;
+  int* d_sc = (int*)ctx->scalars.p;
+  CUDA_TRY(cudaMemsetAsync(d_sc, 0, 16, st));
+  const int maxs = p->match > p->mismatch ? (p->match > p->ambig ? p->match : p->ambig)
+                                          : (p->mismatch > p->ambig ? p->mismatch : p->ambig);
+  PrepArgs pa;
+  pa.roff = b->ref_off; pa.qoff = b->qry_off; pa.n_pairs = P;
+  pa.bl = p->band_left; pa.br = p->band_right; pa.alpha = p->gap_open; pa.beta = p->gap_extend;
+  pa.maxs = maxs;
+  pa.nominal = nominal; pa.iota = (uint32_t*)ctx->iota.p;
+  pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1;
+  const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
+  prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
+  CUDA_TRY(cudaGetLastError());
+  if ((rc = grow(ctx->nominal_sorted, 4 * P))) return rc;
+  size_t tb = ctx->sort_tmp.cap;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(ctx->sort_tmp.p, tb, (const uint32_t*)nominal,
+                                                     (uint32_t*)ctx->nominal_sorted.p,
+                                                     (const uint32_t*)ctx->iota.p, order, (int)P, 0, 32, st));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (ctx->h_scalars[0] & 2) return AGATHA_EEMPTY;
+  if (ctx->h_scalars[0] & 4) return AGATHA_ERANGE;
+  return AGATHA_OK;
+}
+
+int agatha_get_stats(const agatha_ctx_t* ctx, agatha_stats_t* stats) {
+  if (!ctx || !stats) return AGATHA_EINVAL;
+  *stats = ctx->stats;
+  return AGATHA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Every comparison is on all five result fields (score, ref_end, query_end,
+zdrop_antidiag, cells) for every pair: the path is integer work, so the bar is exact
+equality (tests follow SURVEY.md §4 T5/T6/T7).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+SCORING = dict(match=2, mismatch=4, ambig=4, gap_open=4, gap_extend=2)
+
+
+@pytest.fixture(scope="module")
+def ctx(gpu_lib):
+    c = gpu_lib.Context(0)
+    yield c
+    c.close()
+
+
+def compare(gpu_lib, ctx, pairs, params, **kw):
+    got = gpu_lib.align_pairs(ctx, pairs, params, **kw)
+    rc, exp, _ = oracle.align_batch(pairs, params)
+    assert rc == 0
+    bad = np.nonzero(got != exp)[0]
+    if len(bad):
+        k = int(bad[0])
+        R, Q = pairs.pair(k)
+        raise AssertionError(f"{len(bad)}/{len(got)} differ; pair {k} (m={len(R)}, n={len(Q)}) "
+                             f"gpu={got[k]} oracle={exp[k]} params={params}")
+    return got
+
+
+def test_golden_cases_on_gpu(gpu_lib, ctx):
+    from test_oracle import GOLDEN
+    for R, Q, params, expected, cite in GOLDEN:
+        got = gpu_lib.align_pairs(ctx, synth.from_list([(R, Q)]), params)
+        assert tuple(got[0].tolist()) == expected, cite
+
+
+@pytest.mark.parametrize("band", [0, 1, 2, 5, 16, 31, 32, 63, 64, 100, 255, 256, 300, 511])
+def test_random_short_pairs(gpu_lib, ctx, band):
+    rng = np.random.default_rng(1000 + band)
+    pairs = synth.random_short_pairs(rng, 300, 400)
+    for z in (-1, 0, 7, 40):
+        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=band, band_right=band, zdrop=z))
+
+
+def test_asymmetric_bands_and_penalties(gpu_lib, ctx):
+    rng = np.random.default_rng(77)
+    pairs = synth.random_short_pairs(rng, 200, 300)
+    for bl, br in [(0, 7), (7, 0), (3, 60), (200, 17), (500, 500), (-1, 9), (9, -1)]:
+        for (a, b, n, go, ge) in [(2, 4, 4, 4, 2), (1, 3, 1, 6, 2), (3, 5, 0, 7, 7), (2, 4, 4, 0, 0)]:
+            compare(gpu_lib, ctx, pairs, dict(match=a, mismatch=b, ambig=n, gap_open=go,
+                                              gap_extend=ge, band_left=bl, band_right=br, zdrop=25))
+
+
+def test_unbounded_band_short_pairs(gpu_lib, ctx):
+    rng = np.random.default_rng(5)
+    pairs = synth.random_short_pairs(rng, 100, 200)
+    compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=-1, band_right=-1, zdrop=-1))
+    compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=-1, band_right=-1, zdrop=30))
+
+
+def test_edge_corpus(gpu_lib, ctx):
+    lst = [("A", "A"), ("A", "T"), ("N", "N"), ("A", "ACGTACGT" * 10), ("ACGTACGT" * 10, "A"),
+           ("A" * 700, "A" * 3), ("A" * 3, "A" * 700), ("N" * 300, "N" * 300),
+           ("ACGT" * 200, "TGCA" * 200), ("A" * 1000, "A" * 1000), ("AC" * 500, "CA" * 500),
+           ("ACGTTGCA" * 120, "ACGTTGCA" * 119 + "ACG"), ("acgtn" * 50, "ACGTN" * 50)]
+    pairs = synth.from_list(lst)
+    for bl, br in [(0, 0), (1, 1), (3, 2), (100, 100), (511, 511), (0, 511), (511, 0)]:
+        for z in (-1, 0, 5, 100):
+            compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=bl, band_right=br, zdrop=z))
+
+
+def test_tie_heavy_corpus(gpu_lib, ctx):
+    """Poly-A, dinucleotide and tandem repeats: many equal local maxima (readings R5/R6)."""
+    rng = np.random.default_rng(11)
+    lst = []
+    for _ in range(150):
+        unit = "".join(rng.choice(list("ACGT"), int(rng.integers(1, 6))))
+        L = int(rng.integers(20, 600))
+        R = (unit * (L // len(unit) + 1))[:L]
+        Q = (unit * (L // len(unit) + 2))[int(rng.integers(0, 3)):][: int(rng.integers(10, L + 30))]
+        if rng.random() < 0.5:  # break the repeat so Z-drop fires
+            cut = int(rng.integers(1, len(Q)))
+            Q = Q[:cut] + "".join(rng.choice(list("ACGT"), len(Q) - cut))
+        lst.append((R, Q))
+    pairs = synth.from_list(lst)
+    for w in (3, 20, 100):
+        for z in (0, 10, 50):
+            compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=w, band_right=w, zdrop=z))
+
+
+def test_config_c1_full(gpu_lib, ctx):
+    cfg = synth.CONFIGS["C1"]
+    pairs = synth.generate(cfg)
+    got = compare(gpu_lib, ctx, pairs, vars(cfg.scoring))
+    assert (got["zdrop_antidiag"] >= 0).sum() > 30  # Z-drop really exercised
+    # the minimap2 q+e mapping (alpha=6, beta=2) as a second parity pass
+    compare(gpu_lib, ctx, pairs, dict(vars(cfg.scoring), gap_open=6))
+
+
+def test_config_c0(gpu_lib, ctx):
+    cfg = synth.CONFIGS["C0"]
+    pairs = synth.generate(cfg, 0, 3000)
+    rng = np.random.default_rng(0)
+    for _ in range(4):
+        w = int(rng.integers(0, 65))
+        z = int(rng.integers(-1, 51))
+        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=w, band_right=w, zdrop=z))
+
+
+@pytest.mark.parametrize("name,k0,k1", [("C2", 0, 64), ("C3", 0, 24), ("C4", 0, 400), ("C5", 0, 40)])
+def test_config_subsets(gpu_lib, ctx, name, k0, k1):
+    """Pairs of the large configs, shapes as generated (full lengths), vs the oracle."""
+    cfg = synth.CONFIGS[name]
+    pairs = synth.generate(cfg, k0, k1)
+    compare(gpu_lib, ctx, pairs, vars(cfg.scoring))
+
+
+def test_ordering_invariance(gpu_lib, ctx):
+    """Dispatch order (longest-first queue vs input order) never changes a result."""
+    cfg = synth.CONFIGS["C1"]
+    pairs = synth.generate(cfg, 0, 300)
+    a = gpu_lib.align_pairs(ctx, pairs, vars(cfg.scoring))
+    b = gpu_lib.align_pairs(ctx, pairs, vars(cfg.scoring), flags=gpu_lib.ORDER_INPUT)
+    assert a.tobytes() == b.tobytes()
+    # and a pair's result does not depend on its batch mates
+    c = gpu_lib.align_pairs(ctx, pairs.subset([7, 3, 250]), vars(cfg.scoring))
+    assert c.tobytes() == a[[7, 3, 250]].tobytes()
+
+
+def test_device_buffers_and_stream(gpu_lib, ctx):
+    import torch
+    cfg = synth.CONFIGS["C1"]
+    pairs = synth.generate(cfg, 0, 200)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    out = torch.zeros(24 * pairs.n_pairs, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        gpu_lib.align_batch(ctx, dev(pairs.ref), dev(pairs.ref_off.view(np.int64)), dev(pairs.qry),
+                            dev(pairs.qry_off.view(np.int64)), vars(cfg.scoring), out=out, stream=s)
+    got = gpu_lib.device_results(out)
+    rc, exp, _ = oracle.align_batch(pairs, vars(cfg.scoring))
+    assert got.tobytes() == exp.tobytes()
+
+
+def test_localmax_trace_matches_oracle(gpu_lib, ctx):
+    cfg = synth.CONFIGS["C1"]
+    pairs = synth.generate(cfg, 40, 60)
+    params = vars(cfg.scoring)
+    for k in range(pairs.n_pairs):
+        R, Q = pairs.pair(k)
+        cap = len(R) + len(Q) + 1
+        gs, gi = gpu_lib.localmax_trace(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off,
+                                        params, k, cap)
+        rc, res, (os_, oi) = oracle.align_one(R, Q, params, trace=True)
+        c_end = res[3] if res[3] >= 0 else len(R) + len(Q)
+        reached = np.arange(cap) <= c_end
+        assert np.array_equal(gi[reached], oi[reached]), k
+        nonempty = reached & (oi >= 0)
+        assert np.array_equal(gs[nonempty], os_[nonempty]), k
+
+
+def test_pack4_matches_oracle(gpu_lib, ctx):
+    import torch
+    rng = np.random.default_rng(3)
+    for L in (1, 7, 8, 9, 63, 64, 65, 1000, 12345):
+        s = rng.choice(np.frombuffer(b"ACGTNacgtn", np.uint8), L).tobytes()
+        dev = torch.from_numpy(np.frombuffer(s, np.uint8).copy()).cuda()
+        for rev in (False, True):
+            words = torch.zeros((L + 7) // 8, dtype=torch.int32, device="cuda")
+            rc = gpu_lib.pack4(ctx, dev, words, flags=gpu_lib.PACK_REVERSE if rev else 0)
+            assert rc == 0
+            orc, exp = oracle.pack4(s, reverse=rev)
+            assert np.array_equal(words.cpu().numpy().view(np.uint32), exp)
+    bad = torch.from_numpy(np.frombuffer(b"ACGTXACG", np.uint8).copy()).cuda()
+    words = torch.zeros(1, dtype=torch.int32, device="cuda")
+    assert gpu_lib.pack4(ctx, bad, words) == gpu_lib.ECHAR
+    assert gpu_lib.pack4(ctx, bad, words, flags=gpu_lib.N_MAP) == 0
+    assert words.cpu().numpy().view(np.uint32)[0] == oracle.pack4(b"ACGTXACG", n_map=True)[1][0]
+
+
+def test_plan_matches_oracle(gpu_lib, ctx):
+    import torch
+    cfg = synth.CONFIGS["C4"]
+    pairs = synth.generate(cfg, 0, 2000)
+    params = vars(cfg.scoring)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    order = torch.zeros(pairs.n_pairs, dtype=torch.int32, device="cuda")
+    nominal = torch.zeros(pairs.n_pairs, dtype=torch.int32, device="cuda")
+    gpu_lib.plan(ctx, dev(pairs.ref), dev(pairs.ref_off.view(np.int64)), dev(pairs.qry),
+                 dev(pairs.qry_off.view(np.int64)), params, order, nominal)
+    nom = nominal.cpu().numpy().view(np.uint32).astype(np.int64)
+    ordr = order.cpu().numpy().view(np.uint32).astype(np.int64)
+    rl = np.diff(pairs.ref_off.astype(np.int64))
+    ql = np.diff(pairs.qry_off.astype(np.int64))
+    exp = np.array([oracle.nominal_cells(int(m), int(n), 500, 500) for m, n in zip(rl, ql)])
+    assert np.array_equal(nom, exp)
+    assert sorted(ordr.tolist()) == list(range(pairs.n_pairs))      # a permutation
+    assert np.all(np.diff(nom[ordr]) <= 0)                            # longest first
+
+
+def test_error_codes(gpu_lib, ctx):
+    ok = synth.from_list([("ACGT", "ACGT")])
+    with pytest.raises(gpu_lib.AgathaError) as e:
+        gpu_lib.align_pairs(ctx, synth.from_list([("ACGT", "AXGT")]), SCORING)
+    assert e.value.code == gpu_lib.ECHAR
+    got = gpu_lib.align_pairs(ctx, synth.from_list([("ACGT", "AXGT")]), SCORING, flags=gpu_lib.N_MAP)
+    assert tuple(got[0].tolist())[:3] == oracle.align_one("ACGT", "ANGT", SCORING)[1][:3]
+    with pytest.raises(gpu_lib.AgathaError) as e:
+        gpu_lib.align_pairs(ctx, synth.from_list([("ACGT", "")]), SCORING)
+    assert e.value.code == gpu_lib.EEMPTY
+    with pytest.raises(gpu_lib.AgathaError) as e:
+        gpu_lib.align_pairs(ctx, synth.from_list([]), SCORING)
+    assert e.value.code == gpu_lib.EEMPTY
+    for bad in (dict(match=0), dict(mismatch=-1), dict(gap_open=1, gap_extend=2), dict(ambig=-2)):
+        with pytest.raises(gpu_lib.AgathaError) as e:
+            gpu_lib.align_pairs(ctx, ok, dict(SCORING, **bad))
+        assert e.value.code == gpu_lib.EINVAL
+    with pytest.raises(gpu_lib.AgathaError) as e:  # wider than 1024 diagonals
+        gpu_lib.align_pairs(ctx, synth.from_list([("A" * 2000, "A" * 2000)]),
+                            dict(SCORING, band_left=600, band_right=600))
+    assert e.value.code == gpu_lib.ERANGE
+    with pytest.raises(gpu_lib.AgathaError) as e:  # penalty beyond the int8 score table
+        gpu_lib.align_pairs(ctx, ok, dict(SCORING, mismatch=200))
+    assert e.value.code == gpu_lib.ERANGE
