@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark: GCUPS (and alignments/s) of the guided extension aligner on B200.
+
+Contract (the driver's): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
+JSON line on rank 0.  A step is one pass of the whole hot path (SURVEY.md §8(a):
+pack, plan, wavefront alignment with Z-drop, result write; for N > 1 plus the NCCL
+gather of the result records) over one batch of synthetic pairs of BASELINE.json
+configs[1] (C2: 100k HiFi-like pairs of 10-20 kbp, 1% error, band 500, Z-drop 400).
+
+* ``value``      GCUPS of the whole job, inputs resident in HBM when timing starts
+                 (cells = the oracle's algorithmic count, bit-checked in parity);
+* ``e2e``        the same metric through the public C ABI with pinned HOST buffers:
+                 every step copies that step's ASCII inputs in and the result records
+                 out inside the timed region;
+* ``roofline``   the align kernel's integer-op rate vs the ALU issue peak;
+* ``cpu_baseline`` the CPU oracle, as it stands, on a bounded sample of the workload,
+                 on the host cores (rank 0 only).
+
+``--impl reference`` times the oracle itself (the reference arm of this tier).
+Multi-GPU (torchrun): each rank aligns its own shard of pairs (weak scaling: per-GPU
+work fixed), results are gathered with NCCL all_gather; time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+# algorithmic int32 ops per cell and the ALU issue peak.
+OPS_PER_CELL = 10          # Eq. 2 (2), Eq. 3 (2), Eq. 1 (S + add + 2 max), H-alpha (1), Eq. 5 (1)
+SM_COUNT = 148
+LANES_PER_CLK_PER_SM = 128  # 4 SMSP x 1 warp-instruction/clk x 32 lanes (B200_PROFILING / B300_MICROARCH)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--pairs", type=int, default=0, help="pairs per GPU (default: the config's)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample stride (0: auto)")
+    ap.add_argument("--order", default="lpt", choices=["lpt", "input"])
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampling during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": [k for k, v in self.REASONS.items() if self.reasons & v and k != "gpu_idle"],
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_oracle_sample(pairs: synth.Pairs, params: dict, stride: int):
+    """The oracle, as it stands, on every `stride`-th pair; returns (idx, results, seconds)."""
+    import oracle
+    idx = np.arange(0, pairs.n_pairs, stride)
+    sub = pairs.subset(idx)
+    t0 = time.perf_counter()
+    rc, res, _ = oracle.align_batch(sub, params, threads=cpu_cores())
+    dt = time.perf_counter() - t0
+    assert rc == 0, rc
+    return idx, res, dt
+
+
+def reference_arm(args, cfg, rank, world):
+    """--impl reference: the oracle on host cores, each step a bounded sample."""
+    if rank != 0:
+        return
+    n = args.pairs or cfg.n_pairs
+    stride = args.cpu_sample or max(1, n // 150)
+    pairs = synth.generate(cfg.with_pairs(n))
+    params = dict(vars(cfg.scoring))
+    for _ in range(args.warmup):
+        run_oracle_sample(pairs, params, stride * 4)
+    times, cells = [], 0
+    for s in range(args.steps):
+        idx, res, dt = run_oracle_sample(pairs, params, stride)
+        times.append(dt)
+        cells += int(res["cells"].sum())
+    tot = sum(times)
+    value = cells / tot / 1e9
+    line = {
+        "impl": "reference", "metric": "GCUPS", "value": value, "unit": "GCUPS",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": config_dict(cfg, n, world),
+        "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": cpu_cores(), "kind": "oracle",
+                         "sample": f"every {stride}th pair of {n} ({len(idx)} pairs per step)"},
+        "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, n_per_gpu, world):
+    sc = cfg.scoring
+    return {"workload": f"{cfg.name}: {cfg.description}", "pairs_per_gpu": n_per_gpu,
+            "global_pairs": n_per_gpu * world, "band": [sc.band_left, sc.band_right],
+            "zdrop": sc.zdrop,
+            "scoring": {"match": sc.match, "mismatch": sc.mismatch, "ambig": sc.ambig,
+                        "gap_open": sc.gap_open, "gap_extend": sc.gap_extend},
+            "seed": cfg.seed, "parallelism": f"pairs sharded over {world} GPU(s)",
+            "l2": "inputs (GBs of sequence) exceed the 126 MB L2; no flush needed"}
+
+
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[args.config]
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2403_06478_b200 import agatha
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = args.pairs or cfg.n_pairs
+    # rank r aligns pairs [r*n, (r+1)*n) of the config's infinite pair stream (weak scaling)
+    full = cfg.with_pairs(n * world)
+
+    # pinned host buffers (used by the e2e leg); inputs copied once to HBM for `value`
+    def pinned(nr, nq):
+        return (torch.empty(nr, dtype=torch.uint8, pin_memory=True).numpy(),
+                torch.empty(nq, dtype=torch.uint8, pin_memory=True).numpy())
+
+    t0 = time.perf_counter()
+    pairs = synth.generate(full, rank * n, (rank + 1) * n, pinned_out=pinned)
+    gen_s = time.perf_counter() - t0
+    params = dict(vars(cfg.scoring))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    d_ref, d_qry = dev(pairs.ref), dev(pairs.qry)
+    d_roff, d_qoff = dev(pairs.ref_off.view(np.int64)), dev(pairs.qry_off.view(np.int64))
+    d_out = torch.zeros(24 * n, dtype=torch.uint8, device="cuda")
+    gathered = torch.zeros(24 * n * world, dtype=torch.uint8, device="cuda") if world > 1 else None
+    flags = agatha.ORDER_INPUT if args.order == "input" else 0
+    ctx = agatha.Context(local)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        agatha.align_batch(ctx, d_ref, d_roff, d_qry, d_qoff, params, out=d_out, flags=flags,
+                           stream=stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, d_out)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    align_ms = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+            align_ms.append(ctx.stats()["align_ms"])
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    stats = ctx.stats()
+    res = agatha.device_results(d_out)
+    cells_rank = int(res["cells"].sum())
+    t = torch.tensor([ms, float(cells_rank)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+        ms_max, cells_all = float(tmax[0]), float(tsum[1])
+    else:
+        ms_max, cells_all = ms, float(cells_rank)
+    sec = ms_max / 1e3
+    gcups = cells_all * args.steps / sec / 1e9
+    aln_s = n * world * args.steps / sec
+
+    # e2e: the public C ABI with pinned host buffers (H2D of inputs + D2H of results each step)
+    e2e = None
+    if not args.no_e2e:
+        host_out = np.zeros(n, agatha.RESULT_DTYPE)
+        for _ in range(1):
+            agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
+                               out=host_out, flags=flags, stream=stream)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
+                               out=host_out, flags=flags, stream=stream)
+        ev1.record(stream)
+        barrier()
+        e_ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            e_ms = float(te[0])
+        assert host_out.tobytes() == res.tobytes()
+        h2d = int(pairs.ref.nbytes + pairs.qry.nbytes + pairs.ref_off.nbytes + pairs.qry_off.nbytes)
+        e2e = {"value": cells_all * args.steps / (e_ms / 1e3) / 1e9, "unit": "GCUPS",
+               "alignments_per_s": n * world * args.steps / (e_ms / 1e3),
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 24 * n,
+               "ms_per_step": e_ms / args.steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (the align kernel), measured live with CUDA events
+    align_avg_ms = statistics.mean(align_ms)
+    clocks = clk.summary()
+    f_ghz = (clocks["sm_max_mhz"] or 1965) / 1e3
+    peak_tops = SM_COUNT * LANES_PER_CLK_PER_SM * f_ghz * 1e9 / 1e12
+    achieved_tops = OPS_PER_CELL * cells_rank / (align_avg_ms / 1e3) / 1e12
+    roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Tops/s",
+                "frac": achieved_tops / peak_tops, "traffic": None,
+                "kernel": "align_kernel<32>", "kernel_ms": align_avg_ms,
+                "kernel_gcups": cells_rank / (align_avg_ms / 1e3) / 1e9,
+                "ops_per_cell": OPS_PER_CELL,
+                "peak_basis": f"148 SM x 128 int32 lanes/clk (issue limit) x {f_ghz:.3f} GHz (clocks.max.sm)"}
+
+    cpu = None
+    parity = None
+    if not args.no_cpu:
+        stride = args.cpu_sample or max(1, n // 1000)
+        idx, ores, dt = run_oracle_sample(pairs, params, stride)
+        cpu = {"value": float(ores["cells"].sum()) / dt / 1e9, "unit": "GCUPS", "cores": cpu_cores(),
+               "kind": "oracle", "sample": f"every {stride}th pair of rank 0's {n} ({len(idx)} pairs, "
+                                           f"{dt:.1f} s)"}
+        mism = int((res[idx] != ores).sum())
+        parity = {"pairs_checked": int(len(idx)), "mismatches": mism}
+
+    line = {
+        "metric": "GCUPS", "value": gcups, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": config_dict(cfg, n, world), "alignments_per_s": aln_s,
+        "cells_per_step": cells_all, "zdrop_terminated": int((res["zdrop_antidiag"] >= 0).sum()),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": stats["kernel_launches"] * args.steps,
+        "library_launches": stats["library_launches"] * args.steps,
+        "stats_last_step": stats, "clocks": clocks, "parity": parity,
+        "gen_seconds": gen_s,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
