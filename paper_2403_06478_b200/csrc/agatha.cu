@@ -58,6 +58,7 @@ struct AlignArgs {
   int* trace_score;
   int* trace_i;
   long long trace_cap;
+  int sixteen;               // the constant 16, passed at run time (see make_key)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -81,7 +82,13 @@ __device__ __forceinline__ uint32_t load_word(const uint32_t* base, int w, int n
 
 // Packed (score, rank) key for the local max (Eq. 5): max key = max H, and among equal
 // H the smallest t (smallest diagonal inside a lane = smallest i on the anti-diagonal).
-__device__ __forceinline__ int make_key(int h, int t) { return h * 16 + (15 - t); }
+// Computed as an IMAD with a runtime multiplier (always 16) so that it issues on the
+// FMA pipe: the kernel is ALU-pipe bound (profiles/r01_ncu_align_kernel_summary.csv).
+__device__ __forceinline__ int make_key(int h, int t, int sixteen) {
+  int k;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(k) : "r"(h), "r"(sixteen), "r"(15 - t));
+  return k;
+}
 
 struct TrueT { static constexpr bool value = true; };
 struct FalseT { static constexpr bool value = false; };
@@ -143,7 +150,7 @@ __device__ __forceinline__ bool process_antidiag(PairState& s, const AlignArgs& 
 template <int K, int PAR, bool MASKED>
 __device__ __forceinline__ int step_cells(int (&H)[K], int (&Eh)[K], int (&Fh)[K],
                                           const uint32_t (&S)[K / 8], int lane, int nalpha,
-                                          int nbeta, int capT, int tlo, int thi) {
+                                          int nbeta, int capT, int tlo, int thi, int sixteen) {
   // edge exchange: the one neighbour slot that lives in the adjacent lane
   int xH, xEF;
   if (PAR == 0) {
@@ -169,7 +176,7 @@ __device__ __forceinline__ int step_cells(int (&H)[K], int (&Eh)[K], int (&Fh)[K
     const int sub = (int)prmt(S[t >> 2], 0u, sel);         // S(R[i],Q[j]), sign-extended
     int h = __viaddmax_s32(max(e, f), nalpha, H[k] + sub); // Eq. 1
     h = __viaddmin_s32(capT, -k * kCapStep, h);            // padding slots stay below -2^20
-    int key = make_key(h, t);
+    int key = make_key(h, t, sixteen);
     if (MASKED) {
       const bool v = (t >= tlo) && (t <= thi);
       H[k] = v ? h : H[k];
@@ -273,7 +280,7 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
       }
-      const int lk = step_cells<K, 0, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi);
+      const int lk = step_cells<K, 0, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi, A.sixteen);
       const int rH = __reduce_max_sync(kFull, lk >> 4);
       if (process_antidiag<K, 1, TRACE>(s, A, cb - 1, lk_prev, rH_prev, lane, pid)) { stop = true; return; }
       lk_prev = lk;
@@ -293,7 +300,7 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
       }
-      const int lk = step_cells<K, 1, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi);
+      const int lk = step_cells<K, 1, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi, A.sixteen);
       const int rH = __reduce_max_sync(kFull, lk >> 4);
       if (process_antidiag<K, 0, TRACE>(s, A, cb, lk_prev, rH_prev, lane, pid)) { stop = true; return; }
       lk_prev = lk;
@@ -671,7 +678,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   A.roff = d_roff; A.qoff = d_qoff; A.order = d_order; A.bad = (const uint8_t*)ctx->bad.p;
   A.out = d_out; A.queue = d_sc + 2; A.n_pairs = (uint32_t)P;
   A.bl = p->band_left; A.br = p->band_right;
-  A.alpha = p->gap_open; A.beta = p->gap_extend; A.zdrop = p->zdrop;
+  A.alpha = p->gap_open; A.beta = p->gap_extend; A.zdrop = p->zdrop; A.sixteen = 16;
   score_table(p, &A.T0, &A.T1);
   A.trace_pair = trace_pair; A.trace_score = trace_score; A.trace_i = trace_i; A.trace_cap = trace_cap;
   int grid = 0;
