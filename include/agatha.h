@@ -50,6 +50,8 @@ extern "C" {
 #define AGATHA_PACK_REVERSE 8u    /* agatha_pack4 only: pack back to front                */
 #define AGATHA_ORDER_INPUT 16u    /* dispatch pairs in input order instead of longest-first
                                      (ordering ablation; results are identical)           */
+#define AGATHA_FORCE_32BIT 32u    /* use the 32-bit kernel even when the 16-bit packed one is
+                                     exact for these parameters (results are identical)   */
 
 /* Scoring (Eq. 1-4 symbols).  Penalties are POSITIVE numbers. */
 typedef struct {
@@ -96,6 +98,7 @@ typedef struct {
   int32_t grid_blocks; /* persistent grid of the align kernel                            */
   int32_t kernel_launches; /* kernels of this library launched by the call              */
   int32_t library_launches; /* CUB radix-sort kernels launched by the call             */
+  int32_t packed16;    /* 1 if the 16-bit packed (DPX .S16x2) kernel ran, 0 for 32-bit    */
 } agatha_stats_t;
 
 /* Create a context on CUDA device `cuda_device`.  Fails with AGATHA_ECUDA when the

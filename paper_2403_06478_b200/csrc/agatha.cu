@@ -26,6 +26,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "agatha.h"
@@ -59,6 +61,7 @@ struct AlignArgs {
   int* trace_i;
   long long trace_cap;
   int sixteen;               // the constant 16, passed at run time (see make_key)
+  uint32_t T16_0, T16_1;     // 16-bit kernel table: byte x = S + 2*alpha
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -72,7 +75,9 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 // non-N bases, x in 1..3 on a mismatch of two non-N bases, x in 4..7 when either is N
 // (N vs N gives 4).  One LOP3.
 __device__ __forceinline__ uint32_t combine(uint32_t r, uint32_t q) {
-  return (r ^ q) | (r & q & 0x44444444u);
+  uint32_t x;  // LUT 0xBC = (a ^ b) | (a & b & c) with a = r, b = q, c = 0x44444444
+  asm("lop3.b32 %0, %1, %2, %3, 0xBC;" : "=r"(x) : "r"(r), "r"(q), "n"(0x44444444));
+  return x;
 }
 
 __device__ __forceinline__ uint32_t load_word(const uint32_t* base, int w, int nw) {
@@ -374,6 +379,446 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignAr
   }
 }
 
+// ===================================================================================
+// 16-bit packed variant (DPX .S16x2): two cells per instruction.
+//
+// Same wavefront, same per-lane slot ranges, same windows as align_kernel<K>, with
+// K = 2*NREG slots per lane held in NREG 32-bit registers as (slot j | slot j+NREG)
+// half-word pairs, so that a slot's two diagonal neighbours j-1 and j+1 live in the
+// same halves of registers j-1 and j+1 (only registers 0 and NREG-1 need a lane
+// exchange, one PRMT each).  Values are stored relative and shifted:
+//     stored = X + alpha*c - B        (X in {H, E, F}, c the anti-diagonal)
+// The alpha*c shift turns Eq. 1-3 into 4 DPX ops per register (2 cells):
+//     Eh = max(Eh_up + (alpha-beta), H_up)          VIADDMNMX.S16x2
+//     Fh = max(Fh_left + (alpha-beta), H_left)      VIADDMNMX.S16x2
+//     H  = max(H_diag + (S + 2alpha), max(Eh, Fh))  VIMNMX.S16x2 + VIADDMNMX.S16x2
+// B is a per-pair base re-centred on the anti-diagonal max every kRebase16 steps.
+// Exactness: all in-band H of one anti-diagonal lie
+// within alpha + D*(beta + a + max(b,n)) below its max, so with the host-side guard
+// every live value stays in (-16000, 12000) and no half-word add wraps.
+// ===================================================================================
+
+constexpr int kW16 = -28000;       // "-infinity" (walls, E/F of boundary cells)
+constexpr int kCapNeg16 = -20000;  // padding cap
+constexpr int kEmpty16 = -16000;   // lane max at or below: no valid cell on the anti-diagonal
+constexpr int kRebase16 = 32;      // iterations (64 anti-diagonals) between re-centrings
+
+__device__ __forceinline__ uint32_t pack2(int lo, int hi) {
+  return ((uint32_t)lo & 0xFFFFu) | ((uint32_t)hi << 16);
+}
+__device__ __forceinline__ int lo16(uint32_t x) { return (int)(int16_t)(x & 0xFFFFu); }
+__device__ __forceinline__ int hi16(uint32_t x) { return ((int)x) >> 16; }
+__device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vmaxs2(a, b); }
+__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vmins2(a, b); }
+__device__ __forceinline__ uint32_t vaddmax2(uint32_t a, uint32_t b, uint32_t c) {
+  return __viaddmax_s16x2(a, b, c);
+}
+
+struct State16 {
+  int m, n, dlo, D, alpha, beta, zdrop;
+  int B;                      // stored = X + alpha*c - B
+  int G_H, G_c, G_i, G_j, G_d;
+  bool haveG, posValid, haveLast;
+  int snapB, snapPar, snapTlo, snapThi;
+  int lastShifted;            // max H + alpha*c of the last non-empty processed anti-diagonal
+  int term;
+};
+
+// First slot of this lane (in slot order: low halves, then high halves) whose value
+// equals v, among the NREG/2 registers r[] of parity P; 99 if none.
+// Only cells t in [tlo, thi] (in the table) are candidates: held boundary values and
+// out-of-table cells of a masked step must never be taken for the argmax.
+template <int NREG>
+__device__ __forceinline__ int first_slot16(const uint32_t (&r)[NREG / 2], int v, int tlo, int thi) {
+  int first = 99;
+#pragma unroll
+  for (int s = NREG / 2 - 1; s >= 0; --s)
+    if (hi16(r[s]) == v && NREG / 2 + s >= tlo && NREG / 2 + s <= thi) first = NREG / 2 + s;
+#pragma unroll
+  for (int s = NREG / 2 - 1; s >= 0; --s)
+    if (lo16(r[s]) == v && s >= tlo && s <= thi) first = s;
+  return first;
+}
+
+// Warp argmax over first_slot16 results -> diagonal d of the smallest (lane, slot).
+template <int NREG>
+__device__ __forceinline__ int argmax_diag16(int first, int P, int dlo) {
+  const unsigned bal = __ballot_sync(kFull, first < 99);
+  const int ls = __ffs(bal) - 1;
+  const int tt = __shfl_sync(kFull, first, ls);
+  const int slot = (tt < NREG / 2) ? P + 2 * tt : NREG + P + 2 * (tt - NREG / 2);
+  return dlo + ls * (2 * NREG) + slot;
+}
+
+template <int NREG>
+__device__ __forceinline__ void resolve_G16(State16& s, const uint32_t* snap, int lane) {
+  if (s.posValid) return;
+  uint32_t r[NREG / 2];
+#pragma unroll
+  for (int k = 0; k < NREG / 2; ++k) r[k] = snap[k * 32 + lane];
+  const int v = s.G_H + s.alpha * s.G_c - s.snapB;
+  const int d = argmax_diag16<NREG>(first_slot16<NREG>(r, v, s.snapTlo, s.snapThi), s.snapPar, s.dlo);
+  s.G_d = d;
+  s.G_i = (s.G_c + d) >> 1;
+  s.G_j = s.G_c - s.G_i;
+  s.posValid = true;
+}
+
+// Eq. 4 / Eq. 6 for anti-diagonal c (slot parity PARC), whose registers H[PARC+2k] are
+// still intact (relative to the current base s.B); rH is the warp max relative to Bc.
+template <int NREG, int PARC, bool TRACE>
+__device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c, int rH, int Bc,
+                                          int tlo, int thi, const uint32_t (&H)[NREG], int lane,
+                                          uint32_t* snap, long long pid) {
+  if (rH <= kEmpty16) return false;  // empty anti-diagonal (reading R11)
+  const int Hs = rH + Bc - s.alpha * c;
+  s.lastShifted = rH + Bc;
+  s.haveLast = true;
+  const bool upd = !s.haveG || Hs > s.G_H;
+  const bool chk = s.haveG && s.zdrop >= 0 && (s.G_H - Hs > s.zdrop) && (c < s.m + s.n);
+  if (TRACE || chk) {
+    uint32_t r[NREG / 2];
+#pragma unroll
+    for (int k = 0; k < NREG / 2; ++k) r[k] = H[PARC + 2 * k];
+    const int d = argmax_diag16<NREG>(first_slot16<NREG>(r, Hs + s.alpha * c - s.B, tlo, thi), PARC, s.dlo);
+    const int i = (c + d) >> 1, j = c - i;
+    if (TRACE && pid == A.trace_pair && lane == 0 && c < A.trace_cap) {
+      A.trace_score[c] = Hs;
+      A.trace_i[c] = i;
+    }
+    if (chk) {
+      resolve_G16<NREG>(s, snap, lane);
+      if (s.G_i < i && s.G_j < j) {
+        const int gap = d - s.G_d;
+        if (s.G_H - Hs > s.zdrop + s.beta * (gap < 0 ? -gap : gap)) {
+          s.term = c;
+          return true;
+        }
+      }
+    }
+  }
+  if (upd) {
+    // defer the argmax: keep the anti-diagonal's registers (one per lane) in shared memory
+#pragma unroll
+    for (int k = 0; k < NREG / 2; ++k) snap[k * 32 + lane] = H[PARC + 2 * k];
+    s.snapB = s.B;
+    s.snapPar = PARC;
+    s.snapTlo = tlo;
+    s.snapThi = thi;
+    s.G_H = Hs;
+    s.G_c = c;
+    s.posValid = false;
+    s.haveG = true;
+  }
+  return false;
+}
+
+// One anti-diagonal step on the NREG/2 registers of parity PAR.  S2[k] holds the
+// shifted substitution scores (S + 2alpha) of register PAR+2k as a half-word pair.
+template <int NREG, int PAR, bool MASKED>
+__device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], uint32_t (&F)[NREG],
+                                      const uint32_t (&CAP)[NREG], const uint32_t (&S2)[NREG / 2],
+                                      const uint32_t (&BND)[NREG / 2], uint32_t AmB2, int lane,
+                                      int tlo, int thi) {
+  const uint32_t W2 = pack2(kW16, kW16);
+  uint32_t xH, xEF;
+  if (PAR == 0) {  // register 0: (lane-1's slot K-1, own slot NREG-1) from register NREG-1
+    uint32_t sh = __shfl_up_sync(kFull, H[NREG - 1], 1);
+    uint32_t se = __shfl_up_sync(kFull, E[NREG - 1], 1);
+    if (lane == 0) { sh = W2; se = W2; }
+    xH = prmt(sh, H[NREG - 1], 0x5432);
+    xEF = prmt(se, E[NREG - 1], 0x5432);
+  } else {         // register NREG-1: (own slot NREG, lane+1's slot 0) from register 0
+    uint32_t sh = __shfl_down_sync(kFull, H[0], 1);
+    uint32_t sf = __shfl_down_sync(kFull, F[0], 1);
+    if (lane == 31) { sh = W2; sf = W2; }
+    xH = prmt(H[0], sh, 0x5432);
+    xEF = prmt(F[0], sf, 0x5432);
+  }
+  uint32_t lm = W2, prev = W2;
+#pragma unroll
+  for (int k = 0; k < NREG / 2; ++k) {
+    const int j = PAR + 2 * k;
+    const uint32_t hu = (j == 0) ? xH : H[j - 1];
+    const uint32_t eu = (j == 0) ? xEF : E[j - 1];
+    const uint32_t hl = (j == NREG - 1) ? xH : H[j + 1];
+    const uint32_t fl = (j == NREG - 1) ? xEF : F[j + 1];
+    const uint32_t e = vaddmax2(eu, AmB2, hu);                 // Eq. 2 (shifted)
+    const uint32_t f = vaddmax2(fl, AmB2, hl);                 // Eq. 3 (shifted)
+    uint32_t h = vaddmax2(H[j], S2[k], vmax2(e, f));           // Eq. 1 (shifted)
+    h = vmin2(h, CAP[j]);                                      // padding slots stay <= -20000
+    if (MASKED) {
+      const uint32_t M = ((k >= tlo && k <= thi) ? 0x0000FFFFu : 0u) |
+                         ((k + NREG / 2 >= tlo && k + NREG / 2 <= thi) ? 0xFFFF0000u : 0u);
+      H[j] = (h & M) | (BND[k] & ~M);
+      E[j] = (e & M) | (W2 & ~M);
+      F[j] = (f & M) | (W2 & ~M);
+      h = (h & M) | (W2 & ~M);
+    } else {
+      H[j] = h;
+      E[j] = e;
+      F[j] = f;
+    }
+    if (k & 1) lm = __vimax3_s16x2(lm, prev, h); else prev = h;  // Eq. 5, per half
+  }
+  if ((NREG / 2) & 1) lm = vmax2(lm, prev);
+  return max(lo16(lm), hi16(lm));
+}
+
+template <int NREG, bool TRACE>
+__device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap) {
+  constexpr int K = 2 * NREG;        // slots per lane
+  constexpr int NC = NREG;           // cells per step per lane (K/2)
+  const uint64_t r0 = A.roff[pid], q0 = A.qoff[pid];
+  const int m = (int)(A.roff[pid + 1] - r0);
+  const int n = (int)(A.qoff[pid + 1] - q0);
+  if (A.bad[pid]) {
+    if (lane == 0) {
+      agatha_result_t z = {0, 0, 0, -1, 0};
+      A.out[pid] = z;
+    }
+    return;
+  }
+  const uint32_t* Rw = A.rw + (r0 >> 3) + pid;
+  const uint32_t* Qw = A.qw + (q0 >> 3) + pid;
+  const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
+  const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;
+  const int br = (A.br < 0 || A.br > m) ? m : A.br;
+  const int alpha = A.alpha, beta = A.beta;
+
+  State16 s;
+  s.m = m; s.n = n; s.dlo = -bl; s.D = bl + br + 1; s.alpha = alpha; s.beta = beta;
+  s.zdrop = A.zdrop; s.B = 0; s.haveG = false; s.posValid = true; s.haveLast = false;
+  s.G_H = 0; s.G_c = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.snapB = 0; s.snapPar = 0;
+  s.lastShifted = 0; s.term = -1;
+  const int dlo = -bl, D = s.D;
+  const uint32_t AmB2 = pack2(alpha - beta, alpha - beta);
+
+  auto fdiag = [&](int d) { return 2 * min(m, n + d) - d; };
+  const int dhi = br;
+  const int cs = 2 + max(bl, br);
+  const int ce = min(fdiag(dlo), fdiag(dhi));
+  const int dmid = min(max(m - n, dlo), dhi);
+  const int c_last = fdiag(dmid);
+
+  int cb = 2 - (dlo & 1);
+  int u = (cb + dlo) >> 1;
+  // boundary value of diagonal d (reading R2); slots beyond the band hold the cap
+  auto bnd = [&](int d) { const int ad = d < 0 ? -d : d; return d == 0 ? 0 : -(alpha + (ad - 1) * beta); };
+
+  // a3: slot k of register j (j or j+NREG) on diagonal dlo + K*lane + k; a slot of
+  // parity(cb) holds anti-diagonal cb-2, the other parity cb-1 (B = 0).
+  uint32_t H[NREG], E[NREG], F[NREG], CAP[NREG];
+  const uint32_t W2 = pack2(kW16, kW16);
+#pragma unroll
+  for (int j = 0; j < NREG; ++j) {
+    int v2[2], c2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = j + h * NREG, g = K * lane + k, d = dlo + g;
+      const bool valid = g < D;
+      c2[h] = valid ? 32767 : kCapNeg16;
+      const int ci = ((k & 1) == 0) ? cb - 2 : cb - 1;  // (dlo + K*lane) has parity of cb
+      v2[h] = valid ? bnd(d) + alpha * ci : kCapNeg16;
+    }
+    H[j] = pack2(v2[0], v2[1]);
+    CAP[j] = pack2(c2[0], c2[1]);
+    E[j] = W2;
+    F[j] = W2;
+  }
+
+  int rpos = u - 1 + lane * NC;
+  int wR = rpos >> 3, oR = rpos & 7;
+  uint32_t Wr0 = load_word(Rw, wR, nwR), Wr1 = load_word(Rw, wR + 1, nwR),
+           Wr2 = load_word(Rw, wR + 2, nwR), nR = load_word(Rw, wR + 3, nwR);
+  int qpos = n + dlo - u + lane * NC;
+  int wQ = qpos >> 3, oQ = qpos & 7;
+  uint32_t Wq0 = load_word(Qw, wQ, nwQ), Wq1 = load_word(Qw, wQ + 1, nwQ),
+           Wq2 = load_word(Qw, wQ + 2, nwQ), nQ = load_word(Qw, wQ - 1, nwQ);
+
+  const uint32_t T0 = A.T16_0, T1 = A.T16_1;
+  int rH_prev = kEmpty16 - 1, B_prev = 0, tlo_prev = 0, thi_prev = NC - 1;
+  bool stop = false;
+  int iters = 0;
+
+  // substitution pairs (cells t, t+NC/2) of one step, from the nibble windows
+  auto scores = [&](uint32_t (&S2)[NREG / 2], const uint32_t (&Wr)[3], const uint32_t (&qg)[2], int shiftR) {
+    if (NREG == 16) {
+      const uint32_t x0 = combine(__funnelshift_rc(Wr[0], Wr[1], shiftR), qg[0]);
+      const uint32_t x1 = combine(__funnelshift_rc(Wr[1], Wr[2], shiftR), qg[1]);
+      const uint32_t a0 = prmt(T0, T1, x0), a1 = prmt(T0, T1, x0 >> 16);
+      const uint32_t b0 = prmt(T0, T1, x1), b1 = prmt(T0, T1, x1 >> 16);
+#pragma unroll
+      for (int k = 0; k < NREG / 2; ++k) {
+        const uint32_t b = (uint32_t)(k & 3);
+        S2[k] = prmt(k < 4 ? a0 : a1, k < 4 ? b0 : b1, b | ((b | 8) << 4) | ((4 + b) << 8) | (((4 + b) | 8) << 12));
+      }
+    } else {  // NREG == 8: cells 0..7 in one word, pairs (t, t+4)
+      const uint32_t x0 = combine(__funnelshift_rc(Wr[0], Wr[1], shiftR), qg[0]);
+      const uint32_t a0 = prmt(T0, T1, x0), a1 = prmt(T0, T1, x0 >> 16);
+#pragma unroll
+      for (int k = 0; k < NREG / 2; ++k) {
+        const uint32_t b = (uint32_t)k;
+        S2[k] = prmt(a0, a1, b | ((b | 8) << 4) | ((4 + b) << 8) | (((4 + b) | 8) << 12));
+      }
+    }
+  };
+  auto boundary2 = [&](uint32_t (&BND)[NREG / 2], int PAR, int c) {
+#pragma unroll
+    for (int k = 0; k < NREG / 2; ++k) {
+      const int j = PAR + 2 * k;
+      const int d0 = dlo + K * lane + j, d1 = d0 + NREG;
+      int v0 = bnd(d0) + alpha * c - s.B, v1 = bnd(d1) + alpha * c - s.B;
+      v0 = min(max(v0, -30000), 30000);
+      v1 = min(max(v1, -30000), 30000);
+      BND[k] = pack2(v0, v1);
+    }
+  };
+
+  auto iteration = [&](auto masked_tag) {
+    constexpr bool MASKED = decltype(masked_tag)::value;
+    uint32_t qg[2], S2[NREG / 2], BND[NREG / 2];
+    const uint32_t Wq[3] = {Wq0, Wq1, Wq2}, Wr[3] = {Wr0, Wr1, Wr2};
+    qg[0] = __funnelshift_rc(Wq[0], Wq[1], 4 * oQ);
+    qg[1] = __funnelshift_rc(Wq[1], Wq[2], 4 * oQ);
+    // ---- step PAR = 0, anti-diagonal cb ----
+    {
+      scores(S2, Wr, qg, 4 * oR);
+      int tlo = 0, thi = NC;
+      if (MASKED) {
+        const int ib = u + lane * NC, jb = u - dlo - lane * NC;
+        tlo = max(1 - ib, jb - n);
+        thi = min(m - ib, jb - 1);
+        boundary2(BND, 0, cb);
+      }
+      const int lmax = step16<NREG, 0, MASKED>(H, E, F, CAP, S2, BND, AmB2, lane, tlo, thi);
+      const int rH = __reduce_max_sync(kFull, lmax);
+      if (process16<NREG, 1, TRACE>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
+      rH_prev = rH;
+      B_prev = s.B;
+      tlo_prev = MASKED ? tlo : 0;
+      thi_prev = MASKED ? thi : NC - 1;
+    }
+    // ---- step PAR = 1, anti-diagonal cb + 1 ----
+    {
+      scores(S2, Wr, qg, 4 * oR + 4);
+      int tlo = 0, thi = NC;
+      if (MASKED) {
+        const int ib = u + 1 + lane * NC, jb = u - dlo - lane * NC;
+        tlo = max(1 - ib, jb - n);
+        thi = min(m - ib, jb - 1);
+        boundary2(BND, 1, cb + 1);
+      }
+      const int lmax = step16<NREG, 1, MASKED>(H, E, F, CAP, S2, BND, AmB2, lane, tlo, thi);
+      const int rH = __reduce_max_sync(kFull, lmax);
+      if (process16<NREG, 0, TRACE>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
+      rH_prev = rH;
+      B_prev = s.B;
+      tlo_prev = MASKED ? tlo : 0;
+      thi_prev = MASKED ? thi : NC - 1;
+    }
+    cb += 2;
+    ++u;
+    ++oR;
+    --oQ;
+  };
+
+  // Window refills (every 8 iterations for each sequence) and base re-centring happen
+  // between runs of iterations whose count is computed up front, so the hot inner loop
+  // carries no per-iteration refill predicates.
+  auto housekeeping = [&]() {
+    if (oR == 8) {
+      oR = 0;
+      ++wR;
+      Wr0 = Wr1; Wr1 = Wr2; Wr2 = nR;
+      nR = load_word(Rw, wR + 3, nwR);
+    }
+    if (oQ < 0) {
+      oQ = 7;
+      --wQ;
+      Wq2 = Wq1; Wq1 = Wq0; Wq0 = nQ;
+      nQ = load_word(Qw, wQ - 1, nwQ);
+    }
+    if (iters >= kRebase16) {  // re-centre the base on the last anti-diagonal max
+      iters = 0;
+      if (s.haveLast) {
+        const int delta = s.lastShifted - s.B;
+        const uint32_t nd2 = pack2(-delta, -delta);
+#pragma unroll
+        for (int j = 0; j < NREG; ++j) {
+          H[j] = vaddmax2(H[j], nd2, W2);
+          if (j & 1) {  // E/F of the last step's parity are the live ones
+            E[j] = vaddmax2(E[j], nd2, W2);
+            F[j] = vaddmax2(F[j], nd2, W2);
+          }
+        }
+        s.B += delta;
+      }
+    }
+  };
+  // run `total` iterations of one phase
+  auto run_phase = [&](auto masked_tag, int total) {
+    while (!stop && total > 0) {
+      int k = min(8 - oR, oQ + 1);
+      k = min(k, kRebase16 - iters);
+      k = min(k, total);
+      total -= k;
+      iters += k;
+#pragma unroll 1
+      for (int t = 0; t < k; ++t) {
+        iteration(masked_tag);
+        if (stop) break;
+      }
+      housekeeping();
+    }
+  };
+
+  {
+    const int head_end = min(cs, c_last + 1);                 // head: cb < cs (and cb <= c_last)
+    run_phase(TrueT{}, cb < head_end ? (head_end - cb + 1) >> 1 : 0);
+    run_phase(FalseT{}, cb + 1 <= ce ? ((ce - cb + 1) >> 1) : 0);  // steady: cb + 1 <= ce
+    run_phase(TrueT{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);  // tail: cb <= c_last
+  }
+  if (!stop) process16<NREG, 1, TRACE>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
+  resolve_G16<NREG>(s, snap, lane);
+
+  const int c_end = s.term >= 0 ? s.term : m + n;
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int g = K * lane + k;
+    if (g < D) {
+      const int d = dlo + g;
+      const int clo = (d < 0 ? -d : d) + 2;
+      const int hi = min(fdiag(d), c_end);
+      if (hi >= clo) cnt += ((hi - clo) >> 1) + 1;
+    }
+  }
+  cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
+  if (lane == 0) {
+    agatha_result_t r;
+    r.score = s.G_H;
+    r.ref_end = s.G_i;
+    r.query_end = s.G_j;
+    r.zdrop_antidiag = s.term;
+    r.cells = cnt;
+    A.out[pid] = r;
+  }
+}
+
+template <int NREG, bool TRACE>
+__global__ void __launch_bounds__(128, NREG >= 16 ? 3 : 4) align16_kernel(AlignArgs A) {
+  __shared__ uint32_t snap_all[4][NREG / 2 * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(A.queue, 1);
+    q = __shfl_sync(kFull, q, 0);
+    if ((uint32_t)q >= A.n_pairs) break;
+    align_pair16<NREG, TRACE>(A, A.order[q], lane, snap_all[warp]);
+  }
+}
+
 // ---- a1: pack (one warp per pair; R forward, Q reversed) ---------------------------
 
 __device__ __forceinline__ uint32_t base_code(uint8_t ch, bool nmap, int* err) {
@@ -557,6 +1002,48 @@ void score_table(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
     }                                        \
   } while (0)
 
+// 16-bit packed kernel eligibility: the within-anti-
+// diagonal spread of H plus the drift between re-centrings must stay inside the
+// half-word range with margin, and S + 2*alpha must fit the int8 score table.
+bool use16(const agatha_params_t* p, int maxD) {
+  const long long a = p->match, al = p->gap_open, be = p->gap_extend;
+  const long long mx = std::max<long long>(a, std::max<long long>(p->mismatch, p->ambig));
+  const long long spread = al + (long long)maxD * (be + a + mx) + 4 * mx;
+  const long long drift = 70 * (2 * al + mx);
+  if (a + 2 * al > 127 || 2 * al - mx < -128) return false;
+  return spread + drift < 15000 && drift + al + a + 127 < 12000 && maxD <= kMaxSlots;
+}
+
+void score_table16(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
+  uint8_t t[8];
+  const int a2 = 2 * p->gap_open;
+  t[0] = (uint8_t)(int8_t)(p->match + a2);
+  for (int x = 1; x < 4; ++x) t[x] = (uint8_t)(int8_t)(a2 - p->mismatch);
+  for (int x = 4; x < 8; ++x) t[x] = (uint8_t)(int8_t)(a2 - p->ambig);
+  *T0 = t[0] | (t[1] << 8) | (t[2] << 16) | ((uint32_t)t[3] << 24);
+  *T1 = t[4] | (t[5] << 8) | (t[6] << 16) | ((uint32_t)t[7] << 24);
+}
+
+template <int NREG, bool TRACE>
+int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
+  static int occ = -1;
+  if (occ < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align16_kernel<NREG, TRACE>, 128, 0) != cudaSuccess) {
+      cudaGetLastError();
+      occ = 1;
+    }
+    if (occ < 1) occ = 1;
+  }
+  const long long want = (long long)ctx->num_sms * occ;
+  const long long need = ((long long)A.n_pairs + 3) / 4;
+  int grid = (int)(want < need ? want : need);
+  if (grid < 1) grid = 1;
+  *grid_out = grid;
+  align16_kernel<NREG, TRACE><<<grid, 128, 0, st>>>(A);
+  CUDA_TRY(cudaGetLastError());
+  return AGATHA_OK;
+}
+
 template <int K, bool TRACE>
 int launch_align(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
   static int occ = -1;
@@ -680,14 +1167,20 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   A.bl = p->band_left; A.br = p->band_right;
   A.alpha = p->gap_open; A.beta = p->gap_extend; A.zdrop = p->zdrop; A.sixteen = 16;
   score_table(p, &A.T0, &A.T1);
+  score_table16(p, &A.T16_0, &A.T16_1);
   A.trace_pair = trace_pair; A.trace_score = trace_score; A.trace_i = trace_i; A.trace_cap = trace_cap;
   int grid = 0;
   const int K = maxD <= 512 ? 16 : 32;
-  if (trace_pair >= 0) {
-    rc = (K == 16) ? launch_align<16, true>(ctx, A, st, &grid) : launch_align<32, true>(ctx, A, st, &grid);
+  const bool k16 = use16(p, maxD) && !(b->flags & AGATHA_FORCE_32BIT);
+  const bool tr = trace_pair >= 0;
+  if (k16) {
+    if (K == 16) rc = tr ? launch_align16<8, true>(ctx, A, st, &grid) : launch_align16<8, false>(ctx, A, st, &grid);
+    else rc = tr ? launch_align16<16, true>(ctx, A, st, &grid) : launch_align16<16, false>(ctx, A, st, &grid);
   } else {
-    rc = (K == 16) ? launch_align<16, false>(ctx, A, st, &grid) : launch_align<32, false>(ctx, A, st, &grid);
+    if (K == 16) rc = tr ? launch_align<16, true>(ctx, A, st, &grid) : launch_align<16, false>(ctx, A, st, &grid);
+    else rc = tr ? launch_align<32, true>(ctx, A, st, &grid) : launch_align<32, false>(ctx, A, st, &grid);
   }
+  ctx->stats.packed16 = k16 ? 1 : 0;
   if (rc) return rc;
   ++launches;
   CUDA_TRY(cudaEventRecord(ctx->ev[3], st));

@@ -22,8 +22,15 @@ def ctx(gpu_lib):
     c.close()
 
 
-def compare(gpu_lib, ctx, pairs, params, **kw):
-    got = gpu_lib.align_pairs(ctx, pairs, params, **kw)
+@pytest.fixture(params=["auto", "force32"])
+def kflags(request, gpu_lib):
+    """Run a test through the default kernel choice (the 16-bit packed kernel whenever it is
+    exact for the parameters) and through the 32-bit kernel."""
+    return 0 if request.param == "auto" else gpu_lib.FORCE_32BIT
+
+
+def compare(gpu_lib, ctx, pairs, params, flags=0, **kw):
+    got = gpu_lib.align_pairs(ctx, pairs, params, flags=flags, **kw)
     rc, exp, _ = oracle.align_batch(pairs, params)
     assert rc == 0
     bad = np.nonzero(got != exp)[0]
@@ -43,30 +50,31 @@ def test_golden_cases_on_gpu(gpu_lib, ctx):
 
 
 @pytest.mark.parametrize("band", [0, 1, 2, 5, 16, 31, 32, 63, 64, 100, 255, 256, 300, 511])
-def test_random_short_pairs(gpu_lib, ctx, band):
+def test_random_short_pairs(gpu_lib, ctx, kflags, band):
     rng = np.random.default_rng(1000 + band)
     pairs = synth.random_short_pairs(rng, 300, 400)
     for z in (-1, 0, 7, 40):
-        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=band, band_right=band, zdrop=z))
+        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=band, band_right=band, zdrop=z), flags=kflags)
 
 
-def test_asymmetric_bands_and_penalties(gpu_lib, ctx):
+def test_asymmetric_bands_and_penalties(gpu_lib, ctx, kflags):
     rng = np.random.default_rng(77)
     pairs = synth.random_short_pairs(rng, 200, 300)
     for bl, br in [(0, 7), (7, 0), (3, 60), (200, 17), (500, 500), (-1, 9), (9, -1)]:
         for (a, b, n, go, ge) in [(2, 4, 4, 4, 2), (1, 3, 1, 6, 2), (3, 5, 0, 7, 7), (2, 4, 4, 0, 0)]:
             compare(gpu_lib, ctx, pairs, dict(match=a, mismatch=b, ambig=n, gap_open=go,
-                                              gap_extend=ge, band_left=bl, band_right=br, zdrop=25))
+                                              gap_extend=ge, band_left=bl, band_right=br, zdrop=25),
+                    flags=kflags)
 
 
-def test_unbounded_band_short_pairs(gpu_lib, ctx):
+def test_unbounded_band_short_pairs(gpu_lib, ctx, kflags):
     rng = np.random.default_rng(5)
     pairs = synth.random_short_pairs(rng, 100, 200)
-    compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=-1, band_right=-1, zdrop=-1))
-    compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=-1, band_right=-1, zdrop=30))
+    compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=-1, band_right=-1, zdrop=-1), flags=kflags)
+    compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=-1, band_right=-1, zdrop=30), flags=kflags)
 
 
-def test_edge_corpus(gpu_lib, ctx):
+def test_edge_corpus(gpu_lib, ctx, kflags):
     lst = [("A", "A"), ("A", "T"), ("N", "N"), ("A", "ACGTACGT" * 10), ("ACGTACGT" * 10, "A"),
            ("A" * 700, "A" * 3), ("A" * 3, "A" * 700), ("N" * 300, "N" * 300),
            ("ACGT" * 200, "TGCA" * 200), ("A" * 1000, "A" * 1000), ("AC" * 500, "CA" * 500),
@@ -74,10 +82,10 @@ def test_edge_corpus(gpu_lib, ctx):
     pairs = synth.from_list(lst)
     for bl, br in [(0, 0), (1, 1), (3, 2), (100, 100), (511, 511), (0, 511), (511, 0)]:
         for z in (-1, 0, 5, 100):
-            compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=bl, band_right=br, zdrop=z))
+            compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=bl, band_right=br, zdrop=z), flags=kflags)
 
 
-def test_tie_heavy_corpus(gpu_lib, ctx):
+def test_tie_heavy_corpus(gpu_lib, ctx, kflags):
     """Poly-A, dinucleotide and tandem repeats: many equal local maxima (readings R5/R6)."""
     rng = np.random.default_rng(11)
     lst = []
@@ -93,34 +101,47 @@ def test_tie_heavy_corpus(gpu_lib, ctx):
     pairs = synth.from_list(lst)
     for w in (3, 20, 100):
         for z in (0, 10, 50):
-            compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=w, band_right=w, zdrop=z))
+            compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=w, band_right=w, zdrop=z), flags=kflags)
 
 
-def test_config_c1_full(gpu_lib, ctx):
+def test_config_c1_full(gpu_lib, ctx, kflags):
     cfg = synth.CONFIGS["C1"]
     pairs = synth.generate(cfg)
-    got = compare(gpu_lib, ctx, pairs, vars(cfg.scoring))
+    got = compare(gpu_lib, ctx, pairs, vars(cfg.scoring), flags=kflags)
     assert (got["zdrop_antidiag"] >= 0).sum() > 30  # Z-drop really exercised
     # the minimap2 q+e mapping (alpha=6, beta=2) as a second parity pass
-    compare(gpu_lib, ctx, pairs, dict(vars(cfg.scoring), gap_open=6))
+    compare(gpu_lib, ctx, pairs, dict(vars(cfg.scoring), gap_open=6), flags=kflags)
 
 
-def test_config_c0(gpu_lib, ctx):
+def test_config_c0(gpu_lib, ctx, kflags):
     cfg = synth.CONFIGS["C0"]
     pairs = synth.generate(cfg, 0, 3000)
     rng = np.random.default_rng(0)
     for _ in range(4):
         w = int(rng.integers(0, 65))
         z = int(rng.integers(-1, 51))
-        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=w, band_right=w, zdrop=z))
+        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=w, band_right=w, zdrop=z), flags=kflags)
 
 
 @pytest.mark.parametrize("name,k0,k1", [("C2", 0, 64), ("C3", 0, 24), ("C4", 0, 400), ("C5", 0, 40)])
-def test_config_subsets(gpu_lib, ctx, name, k0, k1):
+def test_config_subsets(gpu_lib, ctx, kflags, name, k0, k1):
     """Pairs of the large configs, shapes as generated (full lengths), vs the oracle."""
     cfg = synth.CONFIGS[name]
     pairs = synth.generate(cfg, k0, k1)
-    compare(gpu_lib, ctx, pairs, vars(cfg.scoring))
+    compare(gpu_lib, ctx, pairs, vars(cfg.scoring), flags=kflags)
+
+
+def test_kernel_selection(gpu_lib, ctx):
+    """The 16-bit packed kernel runs for the paper's scoring at w = 500; parameters outside
+    its exactness guard run the 32-bit kernel."""
+    pairs = synth.generate(synth.CONFIGS["C2"], 0, 8)
+    gpu_lib.align_pairs(ctx, pairs, vars(synth.CONFIGS["C2"].scoring))
+    assert ctx.stats()["packed16"] == 1
+    gpu_lib.align_pairs(ctx, pairs, vars(synth.CONFIGS["C2"].scoring), flags=gpu_lib.FORCE_32BIT)
+    assert ctx.stats()["packed16"] == 0
+    big = dict(SCORING, match=40, band_left=500, band_right=500, zdrop=400)
+    compare(gpu_lib, ctx, pairs, big)
+    assert ctx.stats()["packed16"] == 0
 
 
 def test_ordering_invariance(gpu_lib, ctx):
@@ -150,7 +171,7 @@ def test_device_buffers_and_stream(gpu_lib, ctx):
     assert got.tobytes() == exp.tobytes()
 
 
-def test_localmax_trace_matches_oracle(gpu_lib, ctx):
+def test_localmax_trace_matches_oracle(gpu_lib, ctx, kflags):
     cfg = synth.CONFIGS["C1"]
     pairs = synth.generate(cfg, 40, 60)
     params = vars(cfg.scoring)
@@ -158,7 +179,7 @@ def test_localmax_trace_matches_oracle(gpu_lib, ctx):
         R, Q = pairs.pair(k)
         cap = len(R) + len(Q) + 1
         gs, gi = gpu_lib.localmax_trace(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off,
-                                        params, k, cap)
+                                        params, k, cap, flags=kflags)
         rc, res, (os_, oi) = oracle.align_one(R, Q, params, trace=True)
         c_end = res[3] if res[3] >= 0 else len(R) + len(Q)
         reached = np.arange(cap) <= c_end
