@@ -27,6 +27,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <climits>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -415,12 +416,12 @@ __device__ __forceinline__ uint32_t vaddmax2(uint32_t a, uint32_t b, uint32_t c)
 }
 
 struct State16 {
-  int m, n, dlo, D, alpha, beta, zdrop;
+  int m, n, mn, dlo, D, alpha, beta, zdrop;
   int B;                      // stored = X + alpha*c - B
-  int G_H, G_c, G_i, G_j, G_d;
-  bool haveG, posValid, haveLast;
+  int G_H, G_c, G_i, G_j, G_d;  // G_H = INT_MIN/2 until the first cell (no global max yet)
+  int zthr;                   // G_H - Z (INT_MIN when Z is off or there is no G yet)
+  bool posValid;
   int snapB, snapPar, snapTlo, snapThi;
-  int lastShifted;            // max H + alpha*c of the last non-empty processed anti-diagonal
   int term;
 };
 
@@ -466,16 +467,17 @@ __device__ __forceinline__ void resolve_G16(State16& s, const uint32_t* snap, in
 
 // Eq. 4 / Eq. 6 for anti-diagonal c (slot parity PARC), whose registers H[PARC+2k] are
 // still intact (relative to the current base s.B); rH is the warp max relative to Bc.
-template <int NREG, int PARC, bool TRACE>
+// Fast path: three compares and one vote; the argmax work runs only when the global max
+// moves (deferred snapshot) or when Eq. 4 could fire.
+template <int NREG, int PARC, bool TRACE, bool STEADY>
 __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c, int rH, int Bc,
                                           int tlo, int thi, const uint32_t (&H)[NREG], int lane,
                                           uint32_t* snap, long long pid) {
-  if (rH <= kEmpty16) return false;  // empty anti-diagonal (reading R11)
+  const bool nonempty = STEADY || rH > kEmpty16;  // empty anti-diagonals are skipped (R11)
   const int Hs = rH + Bc - s.alpha * c;
-  s.lastShifted = rH + Bc;
-  s.haveLast = true;
-  const bool upd = !s.haveG || Hs > s.G_H;
-  const bool chk = s.haveG && s.zdrop >= 0 && (s.G_H - Hs > s.zdrop) && (c < s.m + s.n);
+  const bool upd = nonempty && Hs > s.G_H;
+  const bool chk = nonempty && Hs < s.zthr && c < s.mn;
+  if (!__any_sync(kFull, upd || chk || (TRACE && nonempty))) return false;
   if (TRACE || chk) {
     uint32_t r[NREG / 2];
 #pragma unroll
@@ -507,8 +509,8 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
     s.snapThi = thi;
     s.G_H = Hs;
     s.G_c = c;
+    s.zthr = s.zdrop >= 0 ? Hs - s.zdrop : INT_MIN;
     s.posValid = false;
-    s.haveG = true;
   }
   return false;
 }
@@ -587,10 +589,10 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   const int alpha = A.alpha, beta = A.beta;
 
   State16 s;
-  s.m = m; s.n = n; s.dlo = -bl; s.D = bl + br + 1; s.alpha = alpha; s.beta = beta;
-  s.zdrop = A.zdrop; s.B = 0; s.haveG = false; s.posValid = true; s.haveLast = false;
-  s.G_H = 0; s.G_c = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.snapB = 0; s.snapPar = 0;
-  s.lastShifted = 0; s.term = -1;
+  s.m = m; s.n = n; s.mn = m + n; s.dlo = -bl; s.D = bl + br + 1; s.alpha = alpha; s.beta = beta;
+  s.zdrop = A.zdrop; s.B = 0; s.posValid = true;
+  s.G_H = INT_MIN / 2; s.G_c = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.zthr = INT_MIN;
+  s.snapB = 0; s.snapPar = 0; s.snapTlo = 0; s.snapThi = 0; s.term = -1;
   const int dlo = -bl, D = s.D;
   const uint32_t AmB2 = pack2(alpha - beta, alpha - beta);
 
@@ -693,7 +695,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
       const int lmax = step16<NREG, 0, MASKED>(H, E, F, CAP, S2, BND, AmB2, lane, tlo, thi);
       const int rH = __reduce_max_sync(kFull, lmax);
-      if (process16<NREG, 1, TRACE>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
+      if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
       B_prev = s.B;
       tlo_prev = MASKED ? tlo : 0;
@@ -711,7 +713,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
       const int lmax = step16<NREG, 1, MASKED>(H, E, F, CAP, S2, BND, AmB2, lane, tlo, thi);
       const int rH = __reduce_max_sync(kFull, lmax);
-      if (process16<NREG, 0, TRACE>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
+      if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
       B_prev = s.B;
       tlo_prev = MASKED ? tlo : 0;
@@ -741,8 +743,8 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     }
     if (iters >= kRebase16) {  // re-centre the base on the last anti-diagonal max
       iters = 0;
-      if (s.haveLast) {
-        const int delta = s.lastShifted - s.B;
+      if (rH_prev > kEmpty16) {
+        const int delta = rH_prev + B_prev - s.B;
         const uint32_t nd2 = pack2(-delta, -delta);
 #pragma unroll
         for (int j = 0; j < NREG; ++j) {
@@ -779,7 +781,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     run_phase(FalseT{}, cb + 1 <= ce ? ((ce - cb + 1) >> 1) : 0);  // steady: cb + 1 <= ce
     run_phase(TrueT{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);  // tail: cb <= c_last
   }
-  if (!stop) process16<NREG, 1, TRACE>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
+  if (!stop) process16<NREG, 1, TRACE, false>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
   resolve_G16<NREG>(s, snap, lane);
 
   const int c_end = s.term >= 0 ? s.term : m + n;
