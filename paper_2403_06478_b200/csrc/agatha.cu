@@ -473,7 +473,9 @@ template <int NREG, int PARC, bool TRACE, bool STEADY>
 __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c, int rH, int Bc,
                                           int tlo, int thi, const uint32_t (&H)[NREG], int lane,
                                           uint32_t* snap, long long pid) {
-  const bool nonempty = STEADY || rH > kEmpty16;  // empty anti-diagonals are skipped (R11)
+  // empty anti-diagonals are skipped (R11); with a one-diagonal band every other
+  // anti-diagonal is empty even in the steady phase, so this is always tested
+  const bool nonempty = rH > kEmpty16;
   const int Hs = rH + Bc - s.alpha * c;
   const bool upd = nonempty && Hs > s.G_H;
   const bool chk = nonempty && Hs < s.zthr && c < s.mn;
