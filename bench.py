@@ -181,6 +181,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2403_06478_b200 import agatha
+    from paper_2403_06478_b200 import dist as adist
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -195,14 +196,14 @@ def main():
                 torch.empty(nq, dtype=torch.uint8, pin_memory=True).numpy())
 
     t0 = time.perf_counter()
-    pairs = synth.generate(full, rank * n, (rank + 1) * n, pinned_out=pinned)
+    k0, k1 = adist.shard_range(n, rank)
+    pairs = synth.generate(full, k0, k1, pinned_out=pinned)
     gen_s = time.perf_counter() - t0
     params = dict(vars(cfg.scoring))
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     d_ref, d_qry = dev(pairs.ref), dev(pairs.qry)
     d_roff, d_qoff = dev(pairs.ref_off.view(np.int64)), dev(pairs.qry_off.view(np.int64))
-    d_out = torch.zeros(24 * n, dtype=torch.uint8, device="cuda")
-    gathered = torch.zeros(24 * n * world, dtype=torch.uint8, device="cuda") if world > 1 else None
+    d_out = torch.zeros(adist.RECORD_BYTES * n, dtype=torch.uint8, device="cuda")
     flags = agatha.ORDER_INPUT if args.order == "input" else 0
     ctx = agatha.Context(local)
     stream = torch.cuda.current_stream()
@@ -211,7 +212,7 @@ def main():
         agatha.align_batch(ctx, d_ref, d_roff, d_qry, d_qoff, params, out=d_out, flags=flags,
                            stream=stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, d_out)
+            adist.gather_results(d_out, world)  # NCCL all_gather of the 24-byte records
 
     def barrier():
         if world > 1:
@@ -235,15 +236,8 @@ def main():
     stats = ctx.stats()
     res = agatha.device_results(d_out)
     cells_rank = int(res["cells"].sum())
-    t = torch.tensor([ms, float(cells_rank)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
-        ms_max, cells_all = float(tmax[0]), float(tsum[1])
-    else:
-        ms_max, cells_all = ms, float(cells_rank)
+    ms_max = adist.max_over_ranks(ms, "cuda", world)
+    cells_all = adist.sum_over_ranks(float(cells_rank), "cuda", world)
     sec = ms_max / 1e3
     gcups = cells_all * args.steps / sec / 1e9
     aln_s = n * world * args.steps / sec
@@ -262,11 +256,7 @@ def main():
                                out=host_out, flags=flags, stream=stream)
         ev1.record(stream)
         barrier()
-        e_ms = ev0.elapsed_time(ev1)
-        if world > 1:
-            te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            e_ms = float(te[0])
+        e_ms = adist.max_over_ranks(ev0.elapsed_time(ev1), "cuda", world)
         assert host_out.tobytes() == res.tobytes()
         h2d = int(pairs.ref.nbytes + pairs.qry.nbytes + pairs.ref_off.nbytes + pairs.qry_off.nbytes)
         e2e = {"value": cells_all * args.steps / (e_ms / 1e3) / 1e9, "unit": "GCUPS",

@@ -1,0 +1,63 @@
+"""Multi-GPU plumbing: pairs shard across ranks; NCCL only gathers results.
+
+The path has no data exchange between pairs (§5.8 l.843-846: independent
+per-GPU processing), so each rank aligns its own shard and the only collective is the
+gather of the fixed 24-byte result records (BASELINE.json north_star: "NCCL over
+NVLink used only to gather results").  Shards are contiguous ranges of the counter-
+based pair stream, so every rank can generate its own inputs (synth/).
+
+This module is plumbing: it never touches sequences or scores.
+"""
+from __future__ import annotations
+
+from typing import Tuple
+
+RECORD_BYTES = 24
+
+
+def shard_range(pairs_per_rank: int, rank: int) -> Tuple[int, int]:
+    """Weak scaling: rank r owns pairs [r*n, (r+1)*n) of the stream."""
+    return rank * pairs_per_rank, (rank + 1) * pairs_per_rank
+
+
+def split_range(n_pairs: int, world: int, rank: int) -> Tuple[int, int]:
+    """Strong scaling: a fixed batch of n_pairs split into contiguous near-equal shards."""
+    base, extra = divmod(n_pairs, world)
+    k0 = rank * base + min(rank, extra)
+    return k0, k0 + base + (1 if rank < extra else 0)
+
+
+def gather_results(local, world: int, group=None):
+    """all_gather the ranks' result buffers (uint8 tensors of 24*n bytes, same n on every
+    rank) into one tensor in rank order.  NCCL on CUDA tensors, gloo on CPU tensors."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return local
+    out = torch.empty(local.numel() * world, dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local, group=group)
+    return out
+
+
+def max_over_ranks(value: float, device, world: int) -> float:
+    """The slowest rank's time (the job's time)."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def sum_over_ranks(value: float, device, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t[0])

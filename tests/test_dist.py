@@ -1,0 +1,84 @@
+"""Multi-process plumbing of the sharded path (CPU, gloo, world_size 2).
+
+Each rank takes its shard of the counter-based pair stream (shard_range), produces its
+result records, and the records are gathered in rank order (gather_results) -- the
+same calls bench.py makes over NCCL.  The per-rank records here come from the oracle
+(test infrastructure), so the gathered buffer must equal the oracle run on the whole
+range in one process.  The max/sum reductions used for the job time are checked too.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2403_06478_b200 import dist as adist
+
+N_PER_RANK = 24
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.CONFIGS["C1"]
+    k0, k1 = adist.shard_range(N_PER_RANK, rank)
+    pairs = synth.generate(cfg.with_pairs(N_PER_RANK * world), k0, k1)
+    rc, res, _ = oracle.align_batch(pairs, vars(cfg.scoring), threads=2)
+    assert rc == 0
+    local = torch.from_numpy(res.view(np.uint8).copy())
+    gathered = adist.gather_results(local, world)
+    tmax = adist.max_over_ranks(float(rank + 1), "cpu", world)
+    tsum = adist.sum_over_ranks(float(res["cells"].sum()), "cpu", world)
+    if rank == 0:
+        np.save(os.path.join(outdir, "gathered.npy"), gathered.numpy())
+        np.save(os.path.join(outdir, "scalars.npy"), np.array([tmax, tsum]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_ranges():
+    assert adist.shard_range(10, 0) == (0, 10) and adist.shard_range(10, 3) == (30, 40)
+    for n, w in [(10, 3), (7, 8), (100, 4), (1, 2)]:
+        parts = [adist.split_range(n, w, r) for r in range(w)]
+        assert parts[0][0] == 0 and parts[-1][1] == n
+        assert all(parts[r][1] == parts[r + 1][0] for r in range(w - 1))
+        sizes = [b - a for a, b in parts]
+        assert max(sizes) - min(sizes) <= 1
+
+
+def test_generation_is_shard_invariant():
+    cfg = synth.CONFIGS["C3"].with_pairs(8)
+    whole = synth.generate(cfg, 0, 8)
+    for r in range(2):
+        k0, k1 = adist.shard_range(4, r)
+        part = synth.generate(cfg, k0, k1)
+        for k in range(k0, k1):
+            assert part.pair(k - k0) == whole.pair(k)
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_gather(tmp_path):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    gathered = np.load(tmp_path / "gathered.npy").view(oracle.RESULT_DTYPE)
+    tmax, tsum = np.load(tmp_path / "scalars.npy")
+    cfg = synth.CONFIGS["C1"]
+    allpairs = synth.generate(cfg.with_pairs(N_PER_RANK * world), 0, N_PER_RANK * world)
+    rc, exp, _ = oracle.align_batch(allpairs, vars(cfg.scoring))
+    assert gathered.tobytes() == exp.tobytes()
+    assert tmax == 2.0
+    assert tsum == float(exp["cells"].sum())
