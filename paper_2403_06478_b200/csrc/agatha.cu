@@ -522,8 +522,7 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
 template <int NREG, int PAR, bool MASKED>
 __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], uint32_t (&F)[NREG],
                                       const uint32_t (&CAP)[NREG], const uint32_t (&S2)[NREG / 2],
-                                      const uint32_t (&BND)[NREG / 2], uint32_t AmB2, int lane,
-                                      int tlo, int thi) {
+                                      uint32_t BND2, uint32_t AmB2, int lane, uint32_t V2) {
   const uint32_t W2 = pack2(kW16, kW16);
   uint32_t xH, xEF;
   if (PAR == 0) {  // register 0: (lane-1's slot K-1, own slot NREG-1) from register NREG-1
@@ -552,9 +551,9 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
     uint32_t h = vaddmax2(H[j], S2[k], vmax2(e, f));           // Eq. 1 (shifted)
     h = vmin2(h, CAP[j]);                                      // padding slots stay <= -20000
     if (MASKED) {
-      const uint32_t M = ((k >= tlo && k <= thi) ? 0x0000FFFFu : 0u) |
-                         ((k + NREG / 2 >= tlo && k + NREG / 2 <= thi) ? 0xFFFF0000u : 0u);
-      H[j] = (h & M) | (BND[k] & ~M);
+      // V2 bit k: cell t = k in the table; bit 16+k: cell t = k + NREG/2 in the table
+      const uint32_t M = ((V2 >> k) & 0x00010001u) * 0xFFFFu;
+      H[j] = (h & M) | (BND2 & ~M);
       E[j] = (e & M) | (W2 & ~M);
       F[j] = (f & M) | (W2 & ~M);
       h = (h & M) | (W2 & ~M);
@@ -667,21 +666,25 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
     }
   };
-  auto boundary2 = [&](uint32_t (&BND)[NREG / 2], int PAR, int c) {
-#pragma unroll
-    for (int k = 0; k < NREG / 2; ++k) {
-      const int j = PAR + 2 * k;
-      const int d0 = dlo + K * lane + j, d1 = d0 + NREG;
-      int v0 = bnd(d0) + alpha * c - s.B, v1 = bnd(d1) + alpha * c - s.B;
-      v0 = min(max(v0, -30000), 30000);
-      v1 = min(max(v1, -30000), 30000);
-      BND[k] = pack2(v0, v1);
-    }
+  // Masked steps: the held value of a cell outside the table.  Only boundary cells
+  // (i = 0 or j = 0) are ever read, and on anti-diagonal c both have the value
+  // H = -(alpha + (c-1) beta) (reading R2), so one broadcast value serves every slot.
+  auto boundary2 = [&](int c) {
+    int v = (c == 0 ? 0 : -(alpha + (c - 1) * beta)) + alpha * c - s.B;
+    v = min(max(v, -30000), 30000);
+    return pack2(v, v);
+  };
+  // bit t (t < NC/2) and bit 16 + t - NC/2 (t >= NC/2) set for the cells t in [tlo, thi]
+  auto valid_bits = [&](int tlo, int thi) {
+    const int lo = max(tlo, 0), hi = min(thi, NC - 1);
+    if (hi < lo) return 0u;
+    const uint32_t v = ((hi >= 31) ? 0xFFFFFFFFu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+    return (v & ((1u << (NC / 2)) - 1u)) | ((v >> (NC / 2)) << 16);
   };
 
   auto iteration = [&](auto masked_tag) {
     constexpr bool MASKED = decltype(masked_tag)::value;
-    uint32_t qg[2], S2[NREG / 2], BND[NREG / 2];
+    uint32_t qg[2], S2[NREG / 2], BND2 = 0u, V2 = 0u;
     const uint32_t Wq[3] = {Wq0, Wq1, Wq2}, Wr[3] = {Wr0, Wr1, Wr2};
     qg[0] = __funnelshift_rc(Wq[0], Wq[1], 4 * oQ);
     qg[1] = __funnelshift_rc(Wq[1], Wq[2], 4 * oQ);
@@ -693,9 +696,10 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         const int ib = u + lane * NC, jb = u - dlo - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
-        boundary2(BND, 0, cb);
+        BND2 = boundary2(cb);
+        V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 0, MASKED>(H, E, F, CAP, S2, BND, AmB2, lane, tlo, thi);
+      const int lmax = step16<NREG, 0, MASKED>(H, E, F, CAP, S2, BND2, AmB2, lane, V2);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -711,9 +715,10 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         const int ib = u + 1 + lane * NC, jb = u - dlo - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
-        boundary2(BND, 1, cb + 1);
+        BND2 = boundary2(cb + 1);
+        V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 1, MASKED>(H, E, F, CAP, S2, BND, AmB2, lane, tlo, thi);
+      const int lmax = step16<NREG, 1, MASKED>(H, E, F, CAP, S2, BND2, AmB2, lane, V2);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
