@@ -37,10 +37,18 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-# algorithmic int32 ops per cell and the ALU issue peak.
-OPS_PER_CELL = 10          # Eq. 2 (2), Eq. 3 (2), Eq. 1 (S + add + 2 max), H-alpha (1), Eq. 5 (1)
+# DESIGN.md §6.1 "Roofline": the path is ALU-pipe bound.  Algorithmic work per cell =
+# the minimal ALU-pipe lane-instruction count on sm_100a with DPX .S16x2 (two cells per
+# lane-instruction): Eq. 2 0.5 + Eq. 3 0.5 + Eq. 1 1.0 (max + fused add/max) + S lookup
+# 0.5 + Eq. 5 running max 0.25 = 2.75.  Peak = 148 SMs x 64 ALU lanes/clk (4 SMSP x 16,
+# B300_MICROARCH "alu-pipe rt_SMSP=2"; measured 62.4-62.5, profiles/r01_dpx16.jsonl) x
+# clocks.max.sm.
+OPS_PER_CELL = 2.75
 SM_COUNT = 148
-LANES_PER_CLK_PER_SM = 128  # 4 SMSP x 1 warp-instruction/clk x 32 lanes (B200_PROFILING / B300_MICROARCH)
+LANES_PER_CLK_PER_SM = 64
+# dram__bytes_read.sum + dram__bytes_write.sum per align launch on the full C2 batch, from
+# one `ncu --set full` capture (profiles/r01_ncu_*_summary.csv); updated per profile.
+TRAFFIC = {"align_kernel<32>": 1.603e9 + 0.0748e9, "align16_kernel<16>": 1.588e9 + 0.0142e9}
 
 
 def parse():
@@ -276,12 +284,16 @@ def main():
     f_ghz = (clocks["sm_max_mhz"] or 1965) / 1e3
     peak_tops = SM_COUNT * LANES_PER_CLK_PER_SM * f_ghz * 1e9 / 1e12
     achieved_tops = OPS_PER_CELL * cells_rank / (align_avg_ms / 1e3) / 1e12
-    roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Tops/s",
-                "frac": achieved_tops / peak_tops, "traffic": None,
-                "kernel": "align_kernel<32>", "kernel_ms": align_avg_ms,
+    kname = "align16_kernel<16>" if stats.get("packed16") else f"align_kernel<{stats['slots_per_lane']}>"
+    roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops,
+                "unit": "T ALU lane-instr/s", "frac": achieved_tops / peak_tops,
+                "traffic": TRAFFIC.get(kname), "traffic_unit": "bytes/launch (ncu dram read+write)",
+                "kernel": kname, "kernel_ms": align_avg_ms,
                 "kernel_gcups": cells_rank / (align_avg_ms / 1e3) / 1e9,
+                "gcups_roof": peak_tops * 1e12 / OPS_PER_CELL / 1e9,
                 "ops_per_cell": OPS_PER_CELL,
-                "peak_basis": f"148 SM x 128 int32 lanes/clk (issue limit) x {f_ghz:.3f} GHz (clocks.max.sm)"}
+                "peak_basis": f"148 SM x 64 ALU lanes/clk x {f_ghz:.3f} GHz (clocks.max.sm); "
+                              "ops_per_cell = minimal DPX .S16x2 ALU lane-instructions per cell"}
 
     cpu = None
     parity = None
