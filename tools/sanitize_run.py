@@ -1,0 +1,30 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck): both kernels,
+the trace path, pack4 and plan on C1 pairs plus an edge corpus."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2403_06478_b200 import agatha  # noqa: E402
+
+ctx = agatha.Context(0)
+cfg = synth.CONFIGS["C1"]
+pairs = synth.generate(cfg, 0, 64)
+edge = synth.from_list([("A", "A"), ("ACGT" * 300, "A"), ("A", "ACGT" * 300), ("N" * 50, "N" * 70),
+                        ("ACGTTGCA" * 100, "ACGTTGCA" * 99)])
+for p in (pairs, edge):
+    for flags in (0, agatha.FORCE_32BIT, agatha.ORDER_INPUT):
+        for prm in (vars(cfg.scoring), dict(vars(cfg.scoring), band_left=500, band_right=500, zdrop=-1),
+                    dict(vars(cfg.scoring), band_left=0, band_right=3)):
+            agatha.align_pairs(ctx, p, prm, flags=flags)
+R, Q = pairs.pair(3)
+agatha.localmax_trace(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, vars(cfg.scoring), 3,
+                      len(R) + len(Q) + 1)
+dev = torch.from_numpy(np.frombuffer(b"ACGTNACGTTTT" * 11, np.uint8).copy()).cuda()
+words = torch.zeros((dev.numel() + 7) // 8, dtype=torch.int32, device="cuda")
+agatha.pack4(ctx, dev, words, flags=agatha.PACK_REVERSE)
+torch.cuda.synchronize()
+print("sanitize workload done")
