@@ -61,7 +61,7 @@ class Config:
     name: str
     n_pairs: int
     seed: int
-    len_dist: int  # 0 uniform, 1 log-uniform, 2 mixture of log-uniforms
+    len_dist: int  # 0 uniform, 1 log-uniform, 2 mixture of log-uniforms, 3 two-point mixture
     lo: float
     hi: float
     err_lo: float
@@ -117,6 +117,16 @@ CONFIGS = {
                  description="10k parity pairs, lengths 1-512, random error"),
 }
 
+
+# NEXT #2: the paper's long/short study (§5.6 l.778-795):
+# 4096 bp long vs 128 bp short reads mixed at a varying long percentage.  The paper
+# gives no band, error or batch size; these use the C4 recipe (5% error, 10% chimeric,
+# w = 500, Z = 400) with 100k pairs.
+for _pct in (1, 5, 10, 25, 50):
+    CONFIGS[f"LS{_pct:02d}"] = Config(
+        f"LS{_pct:02d}", 100_000, 100 + _pct, 3, 128, 128, 0.05, 0.05, _T, _T, _T, 0.1,
+        Scoring(band_left=500, band_right=500, zdrop=400), lo2=4096, hi2=4096, p_long=_pct / 100,
+        description=f"100k pairs, {_pct}% 4096 bp + {100 - _pct}% 128 bp (PAPER.md l.786-788)")
 
 _lib: Optional[ctypes.CDLL] = None
 

@@ -27,7 +27,8 @@
 #include <string.h>
 
 typedef struct {
-  uint32_t len_dist;      /* 0: uniform [lo,hi]; 1: log-uniform [lo,hi]; 2: mixture */
+  uint32_t len_dist;      /* 0: uniform [lo,hi]; 1: log-uniform [lo,hi]; 2: mixture of
+                             log-uniforms; 3: two-point mixture (lo2 w.p. p_long, else lo) */
   uint32_t ref_extra_abs; /* extra reference bases after the read end */
   double lo, hi;          /* length range (short component for the mixture) */
   double lo2, hi2;        /* long component of the mixture (log-uniform) */
@@ -65,6 +66,7 @@ static uint64_t draw_len(const synth_cfg_t* c, uint64_t seed, uint64_t k) {
     if (v < c->p_long) { lo = c->lo2; hi = c->hi2; }
   }
   double L;
+  if (c->len_dist == 3) return (uint64_t)(v < c->p_long ? c->lo2 : c->lo);
   if (logu) L = exp(log(lo) + u * (log(hi) - log(lo)));
   else L = lo + u * (hi - lo + 1.0);
   uint64_t Li = (uint64_t)floor(L);
