@@ -63,6 +63,7 @@ struct AlignArgs {
   long long trace_cap;
   int sixteen;               // the constant 16, passed at run time (see make_key)
   uint32_t T16_0, T16_1;     // 16-bit kernel table: byte x = S + 2*alpha
+  uint32_t k65536;           // the constant 65536, passed at run time (see shr16_fma)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -410,6 +411,19 @@ __device__ __forceinline__ uint32_t pack2(int lo, int hi) {
 __device__ __forceinline__ int lo16(uint32_t x) { return (int)(int16_t)(x & 0xFFFFu); }
 __device__ __forceinline__ int hi16(uint32_t x) { return ((int)x) >> 16; }
 __device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vmaxs2(a, b); }
+// x >> 16 (logical / arithmetic) as the high word of x * 65536 on the FMA pipe: the
+// kernel is ALU-pipe bound and the FMA pipe is ~85% idle.  k65536 is passed at run time
+// so that ptxas cannot strength-reduce the multiply back into an ALU shift.
+__device__ __forceinline__ uint32_t shr16_fma(uint32_t x, uint32_t k65536) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, 0;" : "=r"(d) : "r"(x), "r"(k65536));
+  return d;
+}
+__device__ __forceinline__ int hi16_fma(uint32_t x, uint32_t k65536) {
+  int d;
+  asm("mad.hi.s32 %0, %1, %2, 0;" : "=r"(d) : "r"((int)x), "r"((int)k65536));
+  return d;
+}
 __device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vmins2(a, b); }
 __device__ __forceinline__ uint32_t vaddmax2(uint32_t a, uint32_t b, uint32_t c) {
   return __viaddmax_s16x2(a, b, c);
@@ -522,7 +536,8 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
 template <int NREG, int PAR, bool MASKED>
 __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], uint32_t (&F)[NREG],
                                       const uint32_t (&CAP)[NREG], const uint32_t (&S2)[NREG / 2],
-                                      uint32_t BND2, uint32_t AmB2, int lane, uint32_t V2) {
+                                      uint32_t BND2, uint32_t AmB2, int lane, uint32_t V2,
+                                      uint32_t k65536) {
   const uint32_t W2 = pack2(kW16, kW16);
   uint32_t xH, xEF;
   if (PAR == 0) {  // register 0: (lane-1's slot K-1, own slot NREG-1) from register NREG-1
@@ -565,7 +580,7 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
     if (k & 1) lm = __vimax3_s16x2(lm, prev, h); else prev = h;  // Eq. 5, per half
   }
   if ((NREG / 2) & 1) lm = vmax2(lm, prev);
-  return max(lo16(lm), hi16(lm));
+  return max(lo16(lm), hi16_fma(lm, k65536));
 }
 
 template <int NREG, bool TRACE>
@@ -639,7 +654,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   uint32_t Wq0 = load_word(Qw, wQ, nwQ), Wq1 = load_word(Qw, wQ + 1, nwQ),
            Wq2 = load_word(Qw, wQ + 2, nwQ), nQ = load_word(Qw, wQ - 1, nwQ);
 
-  const uint32_t T0 = A.T16_0, T1 = A.T16_1;
+  const uint32_t T0 = A.T16_0, T1 = A.T16_1, k65536 = A.k65536;
   int rH_prev = kEmpty16 - 1, B_prev = 0, tlo_prev = 0, thi_prev = NC - 1;
   bool stop = false;
   int iters = 0;
@@ -649,8 +664,8 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     if (NREG == 16) {
       const uint32_t x0 = combine(__funnelshift_rc(Wr[0], Wr[1], shiftR), qg[0]);
       const uint32_t x1 = combine(__funnelshift_rc(Wr[1], Wr[2], shiftR), qg[1]);
-      const uint32_t a0 = prmt(T0, T1, x0), a1 = prmt(T0, T1, x0 >> 16);
-      const uint32_t b0 = prmt(T0, T1, x1), b1 = prmt(T0, T1, x1 >> 16);
+      const uint32_t a0 = prmt(T0, T1, x0), a1 = prmt(T0, T1, shr16_fma(x0, k65536));
+      const uint32_t b0 = prmt(T0, T1, x1), b1 = prmt(T0, T1, shr16_fma(x1, k65536));
 #pragma unroll
       for (int k = 0; k < NREG / 2; ++k) {
         const uint32_t b = (uint32_t)(k & 3);
@@ -658,7 +673,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
     } else {  // NREG == 8: cells 0..7 in one word, pairs (t, t+4)
       const uint32_t x0 = combine(__funnelshift_rc(Wr[0], Wr[1], shiftR), qg[0]);
-      const uint32_t a0 = prmt(T0, T1, x0), a1 = prmt(T0, T1, x0 >> 16);
+      const uint32_t a0 = prmt(T0, T1, x0), a1 = prmt(T0, T1, shr16_fma(x0, k65536));
 #pragma unroll
       for (int k = 0; k < NREG / 2; ++k) {
         const uint32_t b = (uint32_t)k;
@@ -699,7 +714,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         BND2 = boundary2(cb);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 0, MASKED>(H, E, F, CAP, S2, BND2, AmB2, lane, V2);
+      const int lmax = step16<NREG, 0, MASKED>(H, E, F, CAP, S2, BND2, AmB2, lane, V2, k65536);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -718,7 +733,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         BND2 = boundary2(cb + 1);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 1, MASKED>(H, E, F, CAP, S2, BND2, AmB2, lane, V2);
+      const int lmax = step16<NREG, 1, MASKED>(H, E, F, CAP, S2, BND2, AmB2, lane, V2, k65536);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -1175,6 +1190,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   A.out = d_out; A.queue = d_sc + 2; A.n_pairs = (uint32_t)P;
   A.bl = p->band_left; A.br = p->band_right;
   A.alpha = p->gap_open; A.beta = p->gap_extend; A.zdrop = p->zdrop; A.sixteen = 16;
+  A.k65536 = 65536u;
   score_table(p, &A.T0, &A.T1);
   score_table16(p, &A.T16_0, &A.T16_1);
   A.trace_pair = trace_pair; A.trace_score = trace_score; A.trace_i = trace_i; A.trace_cap = trace_cap;
