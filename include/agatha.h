@@ -63,7 +63,15 @@ typedef struct {
   int32_t band_left;  /* cells with -band_left <= i - j are computed; < 0 = unbounded   */
   int32_t band_right; /* cells with i - j <= band_right are computed; < 0 = unbounded   */
   int32_t zdrop;      /* Z >= 0; < 0 disables the Z-drop test                           */
+  int32_t variant;    /* 0: the readings of DESIGN.md §2 (default).  Bits select the
+                         minimap2-like alternatives (outside the reference; DESIGN.md §2,
+                         SURVEY.md §8(f) NEXT #4):                                       */
 } agatha_params_t;
+
+#define AGATHA_VAR_GATE_GE 1     /* Eq. 4 gating i' <= i and j' <= j instead of strict <       */
+#define AGATHA_VAR_ORIGIN_MAX 2  /* the global max starts at H(0,0) = 0 at (0,0): a pair whose
+                                    cells all score below 0 reports (0, 0, 0)                */
+#define AGATHA_VAR_CHECK_LAST 4  /* Eq. 4 is also tested at the last anti-diagonal c = m+n  */
 
 /* A batch of n_pairs independent pairs.  Pair k is R = ref[ref_off[k] .. ref_off[k+1])
  * and Q = qry[qry_off[k] .. qry_off[k+1]), ASCII A/C/G/T/N (either case).  The offset

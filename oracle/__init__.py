@@ -39,7 +39,11 @@ class Params(ctypes.Structure):
     _fields_ = [("match", ctypes.c_int32), ("mismatch", ctypes.c_int32),
                 ("ambig", ctypes.c_int32), ("gap_open", ctypes.c_int32),
                 ("gap_extend", ctypes.c_int32), ("band_left", ctypes.c_int32),
-                ("band_right", ctypes.c_int32), ("zdrop", ctypes.c_int32)]
+                ("band_right", ctypes.c_int32), ("zdrop", ctypes.c_int32),
+                ("variant", ctypes.c_int32)]
+
+
+VAR_GATE_GE, VAR_ORIGIN_MAX, VAR_CHECK_LAST = 1, 2, 4
 
 
 class _Result(ctypes.Structure):
@@ -54,9 +58,9 @@ class _Trace(ctypes.Structure):
 
 
 def make_params(match=2, mismatch=4, ambig=None, gap_open=4, gap_extend=2, band_left=-1,
-                band_right=-1, zdrop=-1, **_ignored) -> Params:
+                band_right=-1, zdrop=-1, variant=0, **_ignored) -> Params:
     return Params(match, mismatch, mismatch if ambig is None else ambig, gap_open, gap_extend,
-                  band_left, band_right, zdrop)
+                  band_left, band_right, zdrop, variant)
 
 
 def params_from(obj) -> Params:
@@ -65,8 +69,10 @@ def params_from(obj) -> Params:
         return obj
     if isinstance(obj, dict):
         return make_params(**obj)
-    return make_params(**{k: getattr(obj, k) for k in (
-        "match", "mismatch", "ambig", "gap_open", "gap_extend", "band_left", "band_right", "zdrop")})
+    d = {k: getattr(obj, k) for k in (
+        "match", "mismatch", "ambig", "gap_open", "gap_extend", "band_left", "band_right", "zdrop")}
+    d["variant"] = getattr(obj, "variant", 0)
+    return make_params(**d)
 
 
 _lib: Optional[ctypes.CDLL] = None

@@ -44,7 +44,16 @@ typedef struct {
   int32_t band_left;  /* allow i - j >= -band_left; negative = unbounded      */
   int32_t band_right; /* allow i - j <= band_right; negative = unbounded      */
   int32_t zdrop;      /* Z >= 0; negative = Z-drop disabled                  */
+  int32_t variant;    /* 0 = the readings of DESIGN.md; bits select the minimap2-like
+                         alternatives (outside the reference):
+                         1 = Eq. 4 gating i' <= i, j' <= j (non-strict),
+                         2 = the global max starts at the origin H(0,0) = 0,
+                         4 = Eq. 4 is also tested at c = m+n                 */
 } oracle_params_t;
+
+#define VAR_GATE_GE 1
+#define VAR_ORIGIN_MAX 2
+#define VAR_CHECK_LAST 4
 
 typedef struct {
   int32_t score;          /* H(i',j'), the global max (Eq. 6)                 */
@@ -169,6 +178,9 @@ int oracle_align_one(const uint8_t* R, int64_t m, const uint8_t* Q, int64_t n,
   int have_G = 0;
   int32_t G_H = 0;
   int64_t G_i = 0, G_j = 0;
+  if (p->variant & VAR_ORIGIN_MAX) have_G = 1;  /* G = H(0,0) = 0 at (0,0) */
+  const int gate_ge = (p->variant & VAR_GATE_GE) != 0;
+  const int64_t c_check_end = (p->variant & VAR_CHECK_LAST) ? m + n + 1 : m + n;
   int64_t term = -1, cells = 0;
 
   /* step 4: c = 2, 3, ..., m+n */
@@ -202,7 +214,8 @@ int oracle_align_one(const uint8_t* R, int64_t m, const uint8_t* Q, int64_t n,
     if (any) {
       const int64_t L_j = c - L_i;
       /* 4d: Eq. 4 at this c, with the single (global, local) argmax pair */
-      if (have_G && zdrop_on && c < m + n && G_i < L_i && G_j < L_j) {
+      const int gated = gate_ge ? (G_i <= L_i && G_j <= L_j) : (G_i < L_i && G_j < L_j);
+      if (have_G && zdrop_on && c < c_check_end && gated) {
         const int64_t gap = i64abs((L_i - G_i) - (L_j - G_j));
         if ((int64_t)G_H - (int64_t)L_H > (int64_t)p->zdrop + (int64_t)beta * gap) term = c;
       }

@@ -75,11 +75,15 @@ def path_table(R: str, Q: str, match=2, mismatch=4, ambig=None, gap_open=4, gap_
     return best
 
 
-def result_from_table(table, m: int, n: int, band_left=-1, band_right=-1, gap_extend=2, zdrop=-1):
-    """Apply Eq. 4-6 to a table of H values (interior cells only)."""
+def result_from_table(table, m: int, n: int, band_left=-1, band_right=-1, gap_extend=2, zdrop=-1,
+                      variant=0):
+    """Apply Eq. 4-6 to a table of H values (interior cells only).  ``variant`` bits select
+    the minimap2-like alternatives (1: gating <=, 2: the max starts at the origin,
+    4: Eq. 4 also tested at c = m+n)."""
     bl = band_left if band_left >= 0 else 10 ** 9
     br = band_right if band_right >= 0 else 10 ** 9
-    G = None  # (H, i, j)
+    G = (0, 0, 0) if variant & 2 else None  # (H, i, j)
+    last = m + n + 1 if variant & 4 else m + n
     term = -1
     cells = 0
     for c in range(2, m + n + 1):
@@ -91,7 +95,9 @@ def result_from_table(table, m: int, n: int, band_left=-1, band_right=-1, gap_ex
         vals = [(table[(i, j)], i, j) for (i, j) in diag]
         best_h = max(v[0] for v in vals)
         li, lj = min((i, j) for (h, i, j) in vals if h == best_h)
-        if G is not None and zdrop >= 0 and c < m + n and G[1] < li and G[2] < lj:
+        gated = (G[1] <= li and G[2] <= lj) if (G is not None and variant & 1) else \
+            (G is not None and G[1] < li and G[2] < lj)
+        if G is not None and zdrop >= 0 and c < last and gated:
             if G[0] - best_h > zdrop + gap_extend * abs((li - G[1]) - (lj - G[2])):
                 term = c
         if G is None or best_h > G[0]:
@@ -102,7 +108,7 @@ def result_from_table(table, m: int, n: int, band_left=-1, band_right=-1, gap_ex
 
 
 def align(R: str, Q: str, match=2, mismatch=4, ambig=None, gap_open=4, gap_extend=2,
-          band_left=-1, band_right=-1, zdrop=-1):
+          band_left=-1, band_right=-1, zdrop=-1, variant=0):
     """Full result tuple (score, ref_end, query_end, zdrop_antidiag, cells) by brute force."""
     table = path_table(R, Q, match, mismatch, ambig, gap_open, gap_extend, band_left, band_right)
-    return result_from_table(table, len(R), len(Q), band_left, band_right, gap_extend, zdrop)
+    return result_from_table(table, len(R), len(Q), band_left, band_right, gap_extend, zdrop, variant)

@@ -56,6 +56,7 @@ struct AlignArgs {
   uint32_t n_pairs;
   int bl, br;                // band; negative = unbounded
   int alpha, beta, zdrop;
+  int variant;               // AGATHA_VAR_* bits (0 = the DESIGN.md readings)
   uint32_t T0, T1;           // PRMT score table: byte x = S for code-combination x (0..7)
   long long trace_pair;      // -1: no tracing
   int* trace_score;
@@ -115,7 +116,8 @@ __device__ __forceinline__ bool process_antidiag(PairState& s, const AlignArgs& 
                                                  int rH, int lane, long long pid) {
   if (rH <= kEmptyH) return false;  // empty anti-diagonal: skipped (reading R11)
   const bool upd = !s.haveG || rH > s.G_H;
-  const bool chk = s.haveG && A.zdrop >= 0 && (s.G_H - rH > A.zdrop) && (c < s.m + s.n);
+  const int c_end = (A.variant & AGATHA_VAR_CHECK_LAST) ? s.m + s.n + 1 : s.m + s.n;
+  const bool chk = s.haveG && A.zdrop >= 0 && (s.G_H - rH > A.zdrop) && (c < c_end);
   if (!(upd || chk || TRACE)) return false;
   // argmax: smallest lane holding rH, then its smallest slot (encoded in the key)
   const unsigned bal = __ballot_sync(kFull, (lk >> 4) == rH);
@@ -129,7 +131,9 @@ __device__ __forceinline__ bool process_antidiag(PairState& s, const AlignArgs& 
     A.trace_score[c] = rH;
     A.trace_i[c] = i;
   }
-  if (chk && s.G_i < i && s.G_j < j) {
+  const bool gated = (A.variant & AGATHA_VAR_GATE_GE) ? (s.G_i <= i && s.G_j <= j)
+                                                       : (s.G_i < i && s.G_j < j);
+  if (chk && gated) {
     const int gap = d - s.G_d;
     if (s.G_H - rH > A.zdrop + A.beta * (gap < 0 ? -gap : gap)) {
       s.term = c;
@@ -221,7 +225,8 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
 
   PairState s;
   s.m = m; s.n = n; s.dlo = -bl; s.D = bl + br + 1;
-  s.haveG = false; s.G_H = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.term = -1;
+  s.haveG = (A.variant & AGATHA_VAR_ORIGIN_MAX) != 0;  // G = H(0,0) = 0 at the origin
+  s.G_H = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.term = -1;
   const int dlo = -bl, D = s.D;
 
   // padding cap: slot k of this lane is capped at capT - k*kCapStep
@@ -506,7 +511,9 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
     }
     if (chk) {
       resolve_G16<NREG>(s, snap, lane);
-      if (s.G_i < i && s.G_j < j) {
+      const bool gated = (A.variant & AGATHA_VAR_GATE_GE) ? (s.G_i <= i && s.G_j <= j)
+                                                           : (s.G_i < i && s.G_j < j);
+      if (gated) {
         const int gap = d - s.G_d;
         if (s.G_H - Hs > s.zdrop + s.beta * (gap < 0 ? -gap : gap)) {
           s.term = c;
@@ -605,9 +612,14 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   const int alpha = A.alpha, beta = A.beta;
 
   State16 s;
-  s.m = m; s.n = n; s.mn = m + n; s.dlo = -bl; s.D = bl + br + 1; s.alpha = alpha; s.beta = beta;
+  s.m = m; s.n = n; s.dlo = -bl; s.D = bl + br + 1; s.alpha = alpha; s.beta = beta;
+  s.mn = (A.variant & AGATHA_VAR_CHECK_LAST) ? m + n + 1 : m + n;  // Eq. 4 tested for c < mn
   s.zdrop = A.zdrop; s.B = 0; s.posValid = true;
   s.G_H = INT_MIN / 2; s.G_c = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.zthr = INT_MIN;
+  if (A.variant & AGATHA_VAR_ORIGIN_MAX) {  // G = H(0,0) = 0 at the origin
+    s.G_H = 0;
+    s.zthr = A.zdrop >= 0 ? -A.zdrop : INT_MIN;
+  }
   s.snapB = 0; s.snapPar = 0; s.snapTlo = 0; s.snapThi = 0; s.term = -1;
   const int dlo = -bl, D = s.D;
   const uint32_t AmB2 = pack2(alpha - beta, alpha - beta);
@@ -1004,6 +1016,7 @@ int check_params(const agatha_params_t* p) {
   if (p->match > 127 || p->mismatch > 127 || p->ambig > 127) return AGATHA_ERANGE;
   if (p->gap_open > 65535 || p->zdrop > (1 << 24)) return AGATHA_ERANGE;
   if (p->band_left > 4096 || p->band_right > 4096) return AGATHA_ERANGE;
+  if (p->variant & ~7) return AGATHA_EINVAL;
   return AGATHA_OK;
 }
 
@@ -1190,6 +1203,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   A.out = d_out; A.queue = d_sc + 2; A.n_pairs = (uint32_t)P;
   A.bl = p->band_left; A.br = p->band_right;
   A.alpha = p->gap_open; A.beta = p->gap_extend; A.zdrop = p->zdrop; A.sixteen = 16;
+  A.variant = p->variant;
   A.k65536 = 65536u;
   score_table(p, &A.T0, &A.T1);
   score_table16(p, &A.T16_0, &A.T16_1);

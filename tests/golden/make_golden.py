@@ -50,6 +50,35 @@ CASES = [
 ]
 
 
+# SURVEY.md Appendix B.2 "Alternative" column: the same discriminator inputs under the
+# minimap2-like readings (NEXT #4), selected by the variant bits
+# 1 = non-strict gating, 2 = max starts at the origin, 4 = Eq. 4 also at c = m+n.
+VARIANT_CASES = [
+    ("GCTG", "CT", 2, 3, 4, 2, (0, 0, 0, 4, 5), "SURVEY B.2 #4 alternative: origin counts in the max"),
+    ("CGGACT", "CCTAG", 3, 3, 0, 1, (2, 1, 1, 3, 3), "SURVEY B.2 #8 alternative: non-strict gating"),
+    ("TTA", "GCT", 3, 2, 4, 4, (-4, 1, 1, 6, 9), "SURVEY B.2 #9 alternative: checked at c = m+n"),
+    # the default readings on the same inputs (variant 0) for contrast
+    ("GCTG", "CT", 2, 3, 4, 0, (0, 3, 2, -1, 8), "SURVEY B.2 #4 SPEC reading"),
+    ("CGGACT", "CCTAG", 3, 3, 0, 0, (2, 1, 1, 4, 6), "SURVEY B.2 #8 SPEC reading"),
+    ("TTA", "GCT", 3, 2, 4, 0, (-4, 1, 1, -1, 9), "SURVEY B.2 #9 SPEC reading"),
+]
+
+
+def write_variants():
+    rows = []
+    for R, Q, bl, br, z, var, stated, cite in VARIANT_CASES:
+        got = bruteforce.align(R, Q, match=2, mismatch=4, ambig=4, gap_open=4, gap_extend=2,
+                               band_left=bl, band_right=br, zdrop=z, variant=var)
+        if tuple(got) != tuple(stated):
+            raise SystemExit(f"brute force {got} disagrees with stated {stated} for {R}/{Q} ({cite})")
+        rows.append("\t".join([R, Q, str(bl), str(br), str(z), str(var),
+                               ",".join(str(x) for x in got), cite]))
+    hdr = ("# R\tQ\tband_left\tband_right\tzdrop\tvariant\texpected\tcitation  (scoring 2/4/4/4/2)\n"
+           "# written by tests/golden/make_golden.py (oracle.bruteforce); each row equals SURVEY B.2\n")
+    with open(os.path.join(HERE, "variants.tsv"), "w") as f:
+        f.write(hdr + "\n".join(rows) + "\n")
+
+
 def main():
     rows = []
     for R, Q, bl, br, z, go, amb, stated, cite in CASES:
@@ -66,6 +95,7 @@ def main():
     with open(os.path.join(HERE, "cases.tsv"), "w") as f:
         f.write(hdr + "\n".join(rows) + "\n")
     print(f"wrote {len(rows)} cases")
+    write_variants()
 
 
 if __name__ == "__main__":

@@ -251,3 +251,22 @@ def test_error_codes(gpu_lib, ctx):
     with pytest.raises(gpu_lib.AgathaError) as e:  # penalty beyond the int8 score table
         gpu_lib.align_pairs(ctx, ok, dict(SCORING, mismatch=200))
     assert e.value.code == gpu_lib.ERANGE
+
+
+def test_variant_golden_on_gpu(gpu_lib, ctx, kflags):
+    from test_oracle import VARIANTS
+    for R, Q, params, expected, cite in VARIANTS:
+        got = gpu_lib.align_pairs(ctx, synth.from_list([(R, Q)]), dict(SCORING, **params), flags=kflags)
+        assert tuple(got[0].tolist()) == expected, cite
+
+
+@pytest.mark.parametrize("variant", [1, 2, 4, 7])
+def test_variants_random_and_c1(gpu_lib, ctx, kflags, variant):
+    rng = np.random.default_rng(900 + variant)
+    pairs = synth.random_short_pairs(rng, 200, 300)
+    for w, z in [(5, 0), (32, 20), (300, 40), (-1, 10)]:
+        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=w, band_right=w, zdrop=z, variant=variant),
+                flags=kflags)
+    cfg = synth.CONFIGS["C1"]
+    compare(gpu_lib, ctx, synth.generate(cfg, 0, 300), dict(vars(cfg.scoring), variant=variant),
+            flags=kflags)

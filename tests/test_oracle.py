@@ -265,3 +265,38 @@ def test_validation_errors():
     assert oracle.align_one("", "A", {})[0] == oracle.EEMPTY
     assert oracle.align_one("ACGT", "AXGT", {})[0] == oracle.ECHAR
     assert oracle.align_batch(synth.from_list([]), {})[0] == oracle.EEMPTY
+
+
+def load_variants():
+    rows = []
+    with open(os.path.join(HERE, "golden", "variants.tsv")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            t = line.rstrip("\n").split("\t")
+            bl, br, z, var = map(int, t[2:6])
+            rows.append((t[0], t[1], dict(band_left=bl, band_right=br, zdrop=z, variant=var),
+                         tuple(int(v) for v in t[6].split(",")), t[7]))
+    return rows
+
+
+VARIANTS = load_variants()
+
+
+@pytest.mark.parametrize("R,Q,params,expected,cite", VARIANTS, ids=[v[4][:40] for v in VARIANTS])
+def test_variant_golden(R, Q, params, expected, cite):
+    """The minimap2-like alternatives (NEXT #4) on SURVEY B.2's discriminators."""
+    rc, got = oracle.align_one(R, Q, params)
+    assert rc == 0 and tuple(got) == expected, cite
+
+
+def test_variants_vs_bruteforce_random():
+    rng = np.random.default_rng(4321)
+    for _ in range(300):
+        m, n = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        R = "".join(rng.choice(list("ACGTN"), m, p=[0.24, 0.24, 0.24, 0.24, 0.04]))
+        Q = "".join(rng.choice(list("ACGTN"), n, p=[0.24, 0.24, 0.24, 0.24, 0.04]))
+        p = _rand_params(rng)
+        p["variant"] = int(rng.integers(0, 8))
+        rc, got = oracle.align_one(R, Q, p)
+        assert tuple(got) == tuple(bruteforce.align(R, Q, **p)), (R, Q, p)
