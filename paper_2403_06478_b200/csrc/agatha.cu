@@ -43,10 +43,18 @@ constexpr int kNegKey = -(1 << 30);     // key of a cell outside the table
 constexpr int kEmptyH = -kHLimit;       // lane max H at or below this: no cell on the diagonal
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxSlots = 1024;         // 32 lanes x 32 slots
+constexpr int kMaxChunks = 255;         // input chunks of one call (chunk ids are uint8)
+constexpr uint64_t kChunkBytes = 48ull << 20;  // target ASCII bytes per streamed chunk
 
 struct AlignArgs {
-  const uint32_t* rw;        // packed R words, pair p starts at word (ref_off[p] >> 3) + p
-  const uint32_t* qw;        // packed reversed-Q words, same addressing with qry_off
+  uint32_t* rw;              // packed R words, pair p starts at word (ref_off[p] >> 3) + p
+  uint32_t* qw;              // packed reversed-Q words, same addressing with qry_off
+  const uint8_t* ref_ascii;  // ASCII inputs (device), packed by the align kernel (a1)
+  const uint8_t* qry_ascii;
+  const uint8_t* chunk_of;   // input chunk of each pair
+  const int* ready;          // per-chunk arrival flags (host inputs stream in), or null
+  int* err_flags;            // bit 0: non-ACGTN byte
+  int nmap;                  // AGATHA_N_MAP
   const uint64_t* roff;
   const uint64_t* qoff;
   const uint32_t* order;     // dispatch order (a2)
@@ -83,10 +91,6 @@ __device__ __forceinline__ uint32_t combine(uint32_t r, uint32_t q) {
   return x;
 }
 
-__device__ __forceinline__ uint32_t load_word(const uint32_t* base, int w, int nw) {
-  w = w < 0 ? 0 : (w >= nw ? nw - 1 : w);
-  return __ldg(base + w);
-}
 
 // Packed (score, rank) key for the local max (Eq. 5): max key = max H, and among equal
 // H the smallest t (smallest diagonal inside a lane = smallest i on the anti-diagonal).
@@ -96,6 +100,65 @@ __device__ __forceinline__ int make_key(int h, int t, int sixteen) {
   int k;
   asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(k) : "r"(h), "r"(sixteen), "r"(15 - t));
   return k;
+}
+
+__device__ __forceinline__ uint32_t base_code(uint8_t ch, bool nmap, int* err) {
+  const uint8_t u = ch & 0xDF;  // upper case
+  uint32_t c;
+  if (u == 'A') c = 0;
+  else if (u == 'C') c = 1;
+  else if (u == 'G') c = 2;
+  else if (u == 'T') c = 3;
+  else if (u == 'N') c = 4;
+  else {
+    c = 4;
+    if (!nmap) *err = 1;
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint32_t pack_word(const uint8_t* seq, int64_t len, int64_t w, bool rev,
+                                              bool nmap, int* err) {
+  uint32_t word = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int64_t k = 8 * w + t;
+    if (k < len) {
+      const uint8_t ch = rev ? seq[len - 1 - k] : seq[k];
+      word |= base_code(ch, nmap, err) << (4 * t);
+    }
+  }
+  return word;
+}
+
+// a1 fused into the align kernels: the warp that takes a pair packs its R (forward)
+// and Q (reversed) from ASCII into the packed buffers, after its input chunk has
+// arrived (host inputs stream in chunks that overlap the kernel).
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void pack_pair_fused(const uint8_t* __restrict__ ref, const uint8_t* __restrict__ qry,
+                                                uint64_t r0, uint64_t q0, int m, int n, uint32_t* Rw,
+                                                uint32_t* Qw, const int* ready, int chunk, bool nmap,
+                                                int* err_flags, int lane) {
+  if (ready) {
+    while (ld_acquire(ready + chunk) == 0) __nanosleep(500);
+  }
+  int err = 0;
+  for (int w = lane; w < (m + 7) / 8; w += 32) Rw[w] = pack_word(ref + r0, m, w, false, nmap, &err);
+  for (int w = lane; w < (n + 7) / 8; w += 32) Qw[w] = pack_word(qry + q0, n, w, true, nmap, &err);
+  if (__any_sync(kFull, err) && lane == 0) atomicOr(err_flags, 1);
+  __syncwarp();
+}
+
+// Packed words are written by this kernel (pack_pair_fused), so they are read with
+// plain loads, not through the read-only path.
+__device__ __forceinline__ uint32_t load_word_rw(const uint32_t* base, int w, int nw) {
+  w = w < 0 ? 0 : (w >= nw ? nw - 1 : w);
+  return base[w];
 }
 
 struct TrueT { static constexpr bool value = true; };
@@ -216,9 +279,11 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
     }
     return;
   }
-  const uint32_t* Rw = A.rw + (r0 >> 3) + pid;
-  const uint32_t* Qw = A.qw + (q0 >> 3) + pid;
+  uint32_t* Rw = A.rw + (r0 >> 3) + pid;
+  uint32_t* Qw = A.qw + (q0 >> 3) + pid;
   const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
+  pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
+                  A.nmap != 0, A.err_flags, lane);
   const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;   // diagonals beyond hold no cell
   const int br = (A.br < 0 || A.br > m) ? m : A.br;
   const int alpha = A.alpha, beta = A.beta, nbeta = -A.beta, nalpha = -A.alpha;
@@ -260,12 +325,12 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
   int u = (cb + dlo) >> 1;
   int rpos = u - 1 + lane * (K / 2);          // nibble index of R[i] at t = 0, PAR = 0
   int wR = rpos >> 3, oR = rpos & 7;
-  uint32_t Wr0 = load_word(Rw, wR, nwR), Wr1 = load_word(Rw, wR + 1, nwR),
-           Wr2 = load_word(Rw, wR + 2, nwR), nR = load_word(Rw, wR + 3, nwR);
+  uint32_t Wr0 = load_word_rw(Rw, wR, nwR), Wr1 = load_word_rw(Rw, wR + 1, nwR),
+           Wr2 = load_word_rw(Rw, wR + 2, nwR), nR = load_word_rw(Rw, wR + 3, nwR);
   int qpos = n + dlo - u + lane * (K / 2);    // nibble index of Qrev[x] at t = 0
   int wQ = qpos >> 3, oQ = qpos & 7;
-  uint32_t Wq0 = load_word(Qw, wQ, nwQ), Wq1 = load_word(Qw, wQ + 1, nwQ),
-           Wq2 = load_word(Qw, wQ + 2, nwQ), nQ = load_word(Qw, wQ - 1, nwQ);
+  uint32_t Wq0 = load_word_rw(Qw, wQ, nwQ), Wq1 = load_word_rw(Qw, wQ + 1, nwQ),
+           Wq2 = load_word_rw(Qw, wQ + 2, nwQ), nQ = load_word_rw(Qw, wQ - 1, nwQ);
 
   const uint32_t T0 = A.T0, T1 = A.T1;
   int lk_prev = kNegKey, rH_prev = kEmptyH - 1;  // nothing pending before the first step
@@ -325,13 +390,13 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
       oR = 0;
       ++wR;
       Wr0 = Wr1; Wr1 = Wr2; Wr2 = nR;
-      nR = load_word(Rw, wR + 3, nwR);
+      nR = load_word_rw(Rw, wR + 3, nwR);
     }
     if (--oQ < 0) {
       oQ = 7;
       --wQ;
       Wq2 = Wq1; Wq1 = Wq0; Wq0 = nQ;
-      nQ = load_word(Qw, wQ - 1, nwQ);
+      nQ = load_word_rw(Qw, wQ - 1, nwQ);
     }
   };
 
@@ -604,9 +669,11 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     }
     return;
   }
-  const uint32_t* Rw = A.rw + (r0 >> 3) + pid;
-  const uint32_t* Qw = A.qw + (q0 >> 3) + pid;
+  uint32_t* Rw = A.rw + (r0 >> 3) + pid;
+  uint32_t* Qw = A.qw + (q0 >> 3) + pid;
   const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
+  pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
+                  A.nmap != 0, A.err_flags, lane);
   const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;
   const int br = (A.br < 0 || A.br > m) ? m : A.br;
   const int alpha = A.alpha, beta = A.beta;
@@ -659,12 +726,12 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 
   int rpos = u - 1 + lane * NC;
   int wR = rpos >> 3, oR = rpos & 7;
-  uint32_t Wr0 = load_word(Rw, wR, nwR), Wr1 = load_word(Rw, wR + 1, nwR),
-           Wr2 = load_word(Rw, wR + 2, nwR), nR = load_word(Rw, wR + 3, nwR);
+  uint32_t Wr0 = load_word_rw(Rw, wR, nwR), Wr1 = load_word_rw(Rw, wR + 1, nwR),
+           Wr2 = load_word_rw(Rw, wR + 2, nwR), nR = load_word_rw(Rw, wR + 3, nwR);
   int qpos = n + dlo - u + lane * NC;
   int wQ = qpos >> 3, oQ = qpos & 7;
-  uint32_t Wq0 = load_word(Qw, wQ, nwQ), Wq1 = load_word(Qw, wQ + 1, nwQ),
-           Wq2 = load_word(Qw, wQ + 2, nwQ), nQ = load_word(Qw, wQ - 1, nwQ);
+  uint32_t Wq0 = load_word_rw(Qw, wQ, nwQ), Wq1 = load_word_rw(Qw, wQ + 1, nwQ),
+           Wq2 = load_word_rw(Qw, wQ + 2, nwQ), nQ = load_word_rw(Qw, wQ - 1, nwQ);
 
   const uint32_t T0 = A.T16_0, T1 = A.T16_1, k65536 = A.k65536;
   int rH_prev = kEmpty16 - 1, B_prev = 0, tlo_prev = 0, thi_prev = NC - 1;
@@ -767,13 +834,13 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       oR = 0;
       ++wR;
       Wr0 = Wr1; Wr1 = Wr2; Wr2 = nR;
-      nR = load_word(Rw, wR + 3, nwR);
+      nR = load_word_rw(Rw, wR + 3, nwR);
     }
     if (oQ < 0) {
       oQ = 7;
       --wQ;
       Wq2 = Wq1; Wq1 = Wq0; Wq0 = nQ;
-      nQ = load_word(Qw, wQ - 1, nwQ);
+      nQ = load_word_rw(Qw, wQ - 1, nwQ);
     }
     if (iters >= kRebase16) {  // re-centre the base on the last anti-diagonal max
       iters = 0;
@@ -857,54 +924,6 @@ __global__ void __launch_bounds__(128, NREG >= 16 ? 3 : 4) align16_kernel(AlignA
 
 // ---- a1: pack (one warp per pair; R forward, Q reversed) ---------------------------
 
-__device__ __forceinline__ uint32_t base_code(uint8_t ch, bool nmap, int* err) {
-  const uint8_t u = ch & 0xDF;  // upper case
-  uint32_t c;
-  if (u == 'A') c = 0;
-  else if (u == 'C') c = 1;
-  else if (u == 'G') c = 2;
-  else if (u == 'T') c = 3;
-  else if (u == 'N') c = 4;
-  else {
-    c = 4;
-    if (!nmap) *err = 1;
-  }
-  return c;
-}
-
-__device__ __forceinline__ uint32_t pack_word(const uint8_t* seq, int64_t len, int64_t w, bool rev,
-                                              bool nmap, int* err) {
-  uint32_t word = 0;
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int64_t k = 8 * w + t;
-    if (k < len) {
-      const uint8_t ch = rev ? seq[len - 1 - k] : seq[k];
-      word |= base_code(ch, nmap, err) << (4 * t);
-    }
-  }
-  return word;
-}
-
-__global__ void pack_pairs_kernel(const uint8_t* __restrict__ ref, const uint8_t* __restrict__ qry,
-                                  const uint64_t* __restrict__ roff, const uint64_t* __restrict__ qoff,
-                                  uint64_t n_pairs, uint32_t* __restrict__ rw, uint32_t* __restrict__ qw,
-                                  bool nmap, int* __restrict__ err_flags) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  int err = 0;
-  for (uint64_t p = warp; p < n_pairs; p += nwarps) {
-    const uint64_t r0 = roff[p], q0 = qoff[p];
-    const int64_t m = (int64_t)(roff[p + 1] - r0), n = (int64_t)(qoff[p + 1] - q0);
-    uint32_t* R = rw + (r0 >> 3) + p;
-    uint32_t* Q = qw + (q0 >> 3) + p;
-    for (int64_t w = lane; w < (m + 7) / 8; w += 32) R[w] = pack_word(ref + r0, m, w, false, nmap, &err);
-    for (int64_t w = lane; w < (n + 7) / 8; w += 32) Q[w] = pack_word(qry + q0, n, w, true, nmap, &err);
-  }
-  if (__any_sync(kFull, err) && lane == 0) atomicOr(err_flags, 1);
-}
-
 __global__ void pack_seq_kernel(const uint8_t* __restrict__ seq, uint64_t len, uint32_t* __restrict__ words,
                                 bool rev, bool nmap, int* __restrict__ err_flags) {
   int err = 0;
@@ -927,6 +946,10 @@ struct PrepArgs {
   uint8_t* bad;
   int* err_flags;   // bit 1: empty sequence, bit 2: out of range
   int* max_slots;   // max D over the batch
+  const uint64_t* chunk_first;  // nchunks + 1 pair boundaries of the input chunks
+  int nchunks;
+  uint8_t* chunk_of;            // out: chunk of each pair
+  uint64_t* key64;              // out: dispatch key (chunk << 32) | ~nominal, ascending
 };
 
 __global__ void prep_kernel(PrepArgs P) {
@@ -957,8 +980,18 @@ __global__ void prep_kernel(PrepArgs P) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
     if (lane == 0) {
-      P.nominal[p] = (uint32_t)(cnt > 0xffffffffull ? 0xffffffffull : cnt);
+      const uint32_t nom = (uint32_t)(cnt > 0xffffffffull ? 0xffffffffull : cnt);
+      P.nominal[p] = nom;
       P.iota[p] = (uint32_t)p;
+      if (P.chunk_of) {
+        int lo = 0, hi = P.nchunks - 1;  // last chunk c with chunk_first[c] <= p
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (P.chunk_first[mid] <= p) lo = mid; else hi = mid - 1;
+        }
+        P.chunk_of[p] = (uint8_t)lo;
+        P.key64[p] = ((uint64_t)lo << 32) | (uint64_t)(0xffffffffu - nom);
+      }
       P.bad[p] = (uint8_t)(flag != 0);
       if (flag) atomicOr(P.err_flags, flag);
       else atomicMax(P.max_slots, (int)D);
@@ -987,8 +1020,13 @@ struct agatha_ctx {
   DevBuf results;                                     // staging for host outputs
   DevBuf scalars;                                     // err_flags, max_slots, queue
   DevBuf trace;                                       // trace buffers
+  DevBuf chunk_first, chunk_of, key64, key64_sorted, ready;  // chunked input streaming
   int* h_scalars = nullptr;                           // pinned mirror of scalars
+  int* h_ones = nullptr;                              // pinned 1s (chunk-arrival flags)
+  uint64_t* h_chunk_first = nullptr;                  // pinned chunk boundaries
+  cudaStream_t copy_stream = nullptr;                 // H2D of input chunks
   cudaEvent_t ev[6];
+  cudaEvent_t cev[2];
   agatha_stats_t stats;
 };
 
@@ -1121,6 +1159,11 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   uint64_t tot_r, tot_q;
   const uint8_t *d_ref, *d_qry;
   const uint64_t *d_roff, *d_qoff;
+  // Input chunks: host inputs stream in as contiguous ranges of pairs (~48 MB of ASCII
+  // each) on the copy stream while the align kernel runs; a pair waits for its chunk's
+  // flag.  Device inputs are one chunk that is ready from the start.
+  int nchunks = 1;
+  ctx->h_chunk_first[0] = 0;
   if (dev_in) {
     uint64_t tmp[2];
     CUDA_TRY(cudaMemcpyAsync(&tmp[0], b->ref_off + P, 8, cudaMemcpyDeviceToHost, st));
@@ -1135,26 +1178,42 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     if ((rc = grow(ctx->ref_ascii, tot_r)) || (rc = grow(ctx->qry_ascii, tot_q)) ||
         (rc = grow(ctx->ref_off, 8 * (P + 1))) || (rc = grow(ctx->qry_off, 8 * (P + 1))))
       return rc;
-    CUDA_TRY(cudaMemcpyAsync(ctx->ref_ascii.p, b->ref, tot_r, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(ctx->qry_ascii.p, b->qry, tot_q, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(ctx->ref_off.p, b->ref_off, 8 * (P + 1), cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(ctx->qry_off.p, b->qry_off, 8 * (P + 1), cudaMemcpyHostToDevice, st));
     d_ref = (const uint8_t*)ctx->ref_ascii.p;
     d_qry = (const uint8_t*)ctx->qry_ascii.p;
     d_roff = (const uint64_t*)ctx->ref_off.p;
     d_qoff = (const uint64_t*)ctx->qry_off.p;
+    uint64_t target = kChunkBytes;
+    const uint64_t total = tot_r + tot_q;
+    if (total / target + 2 > (uint64_t)kMaxChunks) target = total / (kMaxChunks - 2) + 1;
+    uint64_t acc = 0;
+    for (uint64_t k = 0; k < P; ++k) {
+      acc += (b->ref_off[k + 1] - b->ref_off[k]) + (b->qry_off[k + 1] - b->qry_off[k]);
+      if (acc >= target && k + 1 < P) {
+        ctx->h_chunk_first[nchunks++] = k + 1;
+        acc = 0;
+      }
+    }
   }
+  ctx->h_chunk_first[nchunks] = P;
   CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
 
   // device scratch
-  size_t sort_bytes = 0;
+  size_t sort_bytes = 0, sort_bytes64 = 0;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const uint32_t*)nullptr,
                                             (uint32_t*)nullptr, (const uint32_t*)nullptr,
                                             (uint32_t*)nullptr, (int)P, 0, 32, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes64, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)P, 0, 40, st);
+  if (sort_bytes64 > sort_bytes) sort_bytes = sort_bytes64;
   if ((rc = grow(ctx->rw, 4 * (tot_r / 8 + P + 2))) || (rc = grow(ctx->qw, 4 * (tot_q / 8 + P + 2))) ||
       (rc = grow(ctx->nominal, 4 * P)) || (rc = grow(ctx->nominal_sorted, 4 * P)) ||
       (rc = grow(ctx->iota, 4 * P)) || (rc = grow(ctx->order, 4 * P)) || (rc = grow(ctx->bad, P)) ||
-      (rc = grow(ctx->sort_tmp, sort_bytes)) || (rc = grow(ctx->scalars, 64)))
+      (rc = grow(ctx->sort_tmp, sort_bytes)) || (rc = grow(ctx->scalars, 64)) ||
+      (rc = grow(ctx->chunk_first, 8 * (kMaxChunks + 1))) || (rc = grow(ctx->chunk_of, P)) ||
+      (rc = grow(ctx->key64, 8 * P)) || (rc = grow(ctx->key64_sorted, 8 * P)) ||
+      (rc = grow(ctx->ready, 4 * kMaxChunks)))
     return rc;
   agatha_result_t* d_out = out;
   if (!dev_out) {
@@ -1162,7 +1221,12 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     d_out = (agatha_result_t*)ctx->results.p;
   }
   int* d_sc = (int*)ctx->scalars.p;  // [0] err_flags [1] max_slots [2] queue
+  int* d_ready = (int*)ctx->ready.p;
   CUDA_TRY(cudaMemsetAsync(d_sc, 0, 16, st));
+  CUDA_TRY(cudaMemcpyAsync(ctx->chunk_first.p, ctx->h_chunk_first, 8 * (nchunks + 1),
+                           cudaMemcpyHostToDevice, st));
+  if (dev_in) CUDA_TRY(cudaMemcpyAsync(d_ready, ctx->h_ones, 4, cudaMemcpyHostToDevice, st));
+  else CUDA_TRY(cudaMemsetAsync(d_ready, 0, 4 * nchunks, st));
 
   const int maxs = p->match > p->mismatch ? (p->match > p->ambig ? p->match : p->ambig)
                                           : (p->mismatch > p->ambig ? p->mismatch : p->ambig);
@@ -1172,19 +1236,21 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   pa.maxs = maxs;
   pa.nominal = (uint32_t*)ctx->nominal.p; pa.iota = (uint32_t*)ctx->iota.p;
   pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1;
+  pa.chunk_first = (const uint64_t*)ctx->chunk_first.p; pa.nchunks = nchunks;
+  pa.chunk_of = (uint8_t*)ctx->chunk_of.p; pa.key64 = (uint64_t*)ctx->key64.p;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
   CUDA_TRY(cudaGetLastError());
-  pack_pairs_kernel<<<prep_blocks, 256, 0, st>>>(d_ref, d_qry, d_roff, d_qoff, P, (uint32_t*)ctx->rw.p,
-                                                 (uint32_t*)ctx->qw.p, nmap, d_sc);
-  CUDA_TRY(cudaGetLastError());
-  int launches = 2, lib_launches = 0;
+  int launches = 1, lib_launches = 0;
   const uint32_t* d_order = (const uint32_t*)ctx->iota.p;
   if (!(b->flags & AGATHA_ORDER_INPUT)) {
+    // a2: longest first within each input chunk (chunk-major): key = (chunk << 32) | ~nominal
+    int end_bit = 32;
+    while ((1 << (end_bit - 32)) < nchunks) ++end_bit;
     size_t tb = ctx->sort_tmp.cap;
-    CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(
-        ctx->sort_tmp.p, tb, (const uint32_t*)ctx->nominal.p, (uint32_t*)ctx->nominal_sorted.p,
-        (const uint32_t*)ctx->iota.p, (uint32_t*)ctx->order.p, (int)P, 0, 32, st));
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(
+        ctx->sort_tmp.p, tb, (const uint64_t*)ctx->key64.p, (uint64_t*)ctx->key64_sorted.p,
+        (const uint32_t*)ctx->iota.p, (uint32_t*)ctx->order.p, (int)P, 0, end_bit, st));
     d_order = (const uint32_t*)ctx->order.p;
     lib_launches = 4;
   }
@@ -1192,13 +1258,14 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   const int err0 = ctx->h_scalars[0], maxD = ctx->h_scalars[1];
-  if (err0 & 1) return AGATHA_ECHAR;
   if (err0 & 2) return AGATHA_EEMPTY;
   if (err0 & 4) return AGATHA_ERANGE;
   CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
 
   AlignArgs A;
-  A.rw = (const uint32_t*)ctx->rw.p; A.qw = (const uint32_t*)ctx->qw.p;
+  A.rw = (uint32_t*)ctx->rw.p; A.qw = (uint32_t*)ctx->qw.p;
+  A.ref_ascii = d_ref; A.qry_ascii = d_qry; A.chunk_of = (const uint8_t*)ctx->chunk_of.p;
+  A.ready = d_ready; A.err_flags = d_sc; A.nmap = nmap ? 1 : 0;
   A.roff = d_roff; A.qoff = d_qoff; A.order = d_order; A.bad = (const uint8_t*)ctx->bad.p;
   A.out = d_out; A.queue = d_sc + 2; A.n_pairs = (uint32_t)P;
   A.bl = p->band_left; A.br = p->band_right;
@@ -1222,12 +1289,33 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   ctx->stats.packed16 = k16 ? 1 : 0;
   if (rc) return rc;
   ++launches;
+  if (!dev_in) {
+    // stream the ASCII in chunk by chunk while the kernel runs; each chunk's flag is
+    // written after its bytes (same stream), and the kernel reads it with acquire
+    CUDA_TRY(cudaEventRecord(ctx->cev[0], ctx->copy_stream));
+    for (int c = 0; c < nchunks; ++c) {
+      const uint64_t k0 = ctx->h_chunk_first[c], k1 = ctx->h_chunk_first[c + 1];
+      const uint64_t rb = b->ref_off[k0], re = b->ref_off[k1], qb = b->qry_off[k0], qe = b->qry_off[k1];
+      if (re > rb)
+        CUDA_TRY(cudaMemcpyAsync((uint8_t*)ctx->ref_ascii.p + rb, b->ref + rb, re - rb,
+                                 cudaMemcpyHostToDevice, ctx->copy_stream));
+      if (qe > qb)
+        CUDA_TRY(cudaMemcpyAsync((uint8_t*)ctx->qry_ascii.p + qb, b->qry + qb, qe - qb,
+                                 cudaMemcpyHostToDevice, ctx->copy_stream));
+      CUDA_TRY(cudaMemcpyAsync(d_ready + c, ctx->h_ones, 4, cudaMemcpyHostToDevice, ctx->copy_stream));
+    }
+    CUDA_TRY(cudaEventRecord(ctx->cev[1], ctx->copy_stream));
+  }
   CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
   if (!dev_out)
     CUDA_TRY(cudaMemcpyAsync(out, d_out, sizeof(agatha_result_t) * P, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaEventRecord(ctx->ev[4], st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  cudaEventElapsedTime(&ctx->stats.h2d_ms, ctx->ev[0], ctx->ev[1]);
+  if (!dev_in) CUDA_TRY(cudaStreamSynchronize(ctx->copy_stream));
+  CUDA_TRY(cudaMemcpy(ctx->h_scalars, d_sc, 4, cudaMemcpyDeviceToHost));
+  if (ctx->h_scalars[0] & 1) return AGATHA_ECHAR;  // set by the fused pack (a1)
+  if (dev_in) cudaEventElapsedTime(&ctx->stats.h2d_ms, ctx->ev[0], ctx->ev[1]);
+  else cudaEventElapsedTime(&ctx->stats.h2d_ms, ctx->cev[0], ctx->cev[1]);
   cudaEventElapsedTime(&ctx->stats.prep_ms, ctx->ev[1], ctx->ev[2]);
   cudaEventElapsedTime(&ctx->stats.align_ms, ctx->ev[2], ctx->ev[3]);
   cudaEventElapsedTime(&ctx->stats.d2h_ms, ctx->ev[3], ctx->ev[4]);
@@ -1273,10 +1361,15 @@ int agatha_ctx_create(agatha_ctx_t** out, int device) {
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
   for (int i = 0; i < 6; ++i) cudaEventCreate(&ctx->ev[i]);
-  if (cudaMallocHost(&ctx->h_scalars, 64) != cudaSuccess) {
+  for (int i = 0; i < 2; ++i) cudaEventCreate(&ctx->cev[i]);
+  cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  if (cudaMallocHost(&ctx->h_scalars, 64) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_ones, 4 * kMaxChunks) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_chunk_first, 8 * (kMaxChunks + 1)) != cudaSuccess) {
     delete ctx;
     return AGATHA_ENOMEM;
   }
+  for (int i = 0; i < kMaxChunks; ++i) ctx->h_ones[i] = 1;
   *out = ctx;
   return AGATHA_OK;
 }
@@ -1286,11 +1379,16 @@ void agatha_ctx_destroy(agatha_ctx_t* ctx) {
   cudaSetDevice(ctx->device);
   DevBuf* bufs[] = {&ctx->ref_ascii, &ctx->qry_ascii, &ctx->ref_off, &ctx->qry_off, &ctx->rw,
                     &ctx->qw, &ctx->nominal, &ctx->nominal_sorted, &ctx->iota, &ctx->order,
-                    &ctx->bad, &ctx->sort_tmp, &ctx->results, &ctx->scalars, &ctx->trace};
+                    &ctx->bad, &ctx->sort_tmp, &ctx->results, &ctx->scalars, &ctx->trace,
+                    &ctx->chunk_first, &ctx->chunk_of, &ctx->key64, &ctx->key64_sorted, &ctx->ready};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (int i = 0; i < 6; ++i) cudaEventDestroy(ctx->ev[i]);
+  for (int i = 0; i < 2; ++i) cudaEventDestroy(ctx->cev[i]);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
+  if (ctx->h_ones) cudaFreeHost(ctx->h_ones);
+  if (ctx->h_chunk_first) cudaFreeHost(ctx->h_chunk_first);
   delete ctx;
 }
 
@@ -1367,6 +1465,7 @@ int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* b, const agatha_params_
   pa.maxs = maxs;
   pa.nominal = nominal; pa.iota = (uint32_t*)ctx->iota.p;
   pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1;
+  pa.chunk_first = nullptr; pa.nchunks = 1; pa.chunk_of = nullptr; pa.key64 = nullptr;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
   CUDA_TRY(cudaGetLastError());
