@@ -48,7 +48,7 @@ SM_COUNT = 148
 LANES_PER_CLK_PER_SM = 64
 # dram__bytes_read.sum + dram__bytes_write.sum per align launch on the full C2 batch, from
 # one `ncu --set full` capture (profiles/r01_ncu_*_summary.csv); updated per profile.
-TRAFFIC = {"align_kernel<32>": 1.603e9 + 0.0748e9, "align16_kernel<16>": 1.588e9 + 0.0142e9}
+TRAFFIC = {"align_kernel<32>": 1.603e9 + 0.0748e9, "align16_kernel<16>": 3.346e9 + 1.505e9}
 
 
 def parse():
