@@ -161,6 +161,7 @@ __device__ __forceinline__ uint32_t load_word_rw(const uint32_t* base, int w, in
   return base[w];
 }
 
+template <int M> struct Mode { static constexpr int value = M; };
 struct TrueT { static constexpr bool value = true; };
 struct FalseT { static constexpr bool value = false; };
 
@@ -605,7 +606,11 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
 
 // One anti-diagonal step on the NREG/2 registers of parity PAR.  S2[k] holds the
 // shifted substitution scores (S + 2alpha) of register PAR+2k as a half-word pair.
-template <int NREG, int PAR, bool MASKED>
+// MODE 0: steady (every band slot in the table); 1: head (cells before the table hold
+// the boundary value, E/F = -infinity, and are excluded from the max); 2: tail (cells
+// past the table end are never read by a valid cell, so they are only excluded from
+// the max).
+template <int NREG, int PAR, int MODE>
 __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], uint32_t (&F)[NREG],
                                       const uint32_t (&CAP)[NREG], const uint32_t (&S2)[NREG / 2],
                                       uint32_t BND2, uint32_t AmB2, int lane, uint32_t V2,
@@ -637,12 +642,18 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
     const uint32_t f = vaddmax2(fl, AmB2, hl);                 // Eq. 3 (shifted)
     uint32_t h = vaddmax2(H[j], S2[k], vmax2(e, f));           // Eq. 1 (shifted)
     h = vmin2(h, CAP[j]);                                      // padding slots stay <= -20000
-    if (MASKED) {
+    if (MODE == 1) {
       // V2 bit k: cell t = k in the table; bit 16+k: cell t = k + NREG/2 in the table
       const uint32_t M = ((V2 >> k) & 0x00010001u) * 0xFFFFu;
       H[j] = (h & M) | (BND2 & ~M);
       E[j] = (e & M) | (W2 & ~M);
       F[j] = (f & M) | (W2 & ~M);
+      h = (h & M) | (W2 & ~M);
+    } else if (MODE == 2) {
+      const uint32_t M = ((V2 >> k) & 0x00010001u) * 0xFFFFu;
+      H[j] = h;
+      E[j] = e;
+      F[j] = f;
       h = (h & M) | (W2 & ~M);
     } else {
       H[j] = h;
@@ -776,8 +787,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     return (v & ((1u << (NC / 2)) - 1u)) | ((v >> (NC / 2)) << 16);
   };
 
-  auto iteration = [&](auto masked_tag) {
-    constexpr bool MASKED = decltype(masked_tag)::value;
+  auto iteration = [&](auto mode_tag) {
+    constexpr int MODE = decltype(mode_tag)::value;
+    constexpr bool MASKED = MODE != 0;
     uint32_t qg[2], S2[NREG / 2], BND2 = 0u, V2 = 0u;
     const uint32_t Wq[3] = {Wq0, Wq1, Wq2}, Wr[3] = {Wr0, Wr1, Wr2};
     qg[0] = __funnelshift_rc(Wq[0], Wq[1], 4 * oQ);
@@ -790,10 +802,10 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         const int ib = u + lane * NC, jb = u - dlo - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
-        BND2 = boundary2(cb);
+        if (MODE == 1) BND2 = boundary2(cb);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 0, MASKED>(H, E, F, CAP, S2, BND2, AmB2, lane, V2, k65536);
+      const int lmax = step16<NREG, 0, MODE>(H, E, F, CAP, S2, BND2, AmB2, lane, V2, k65536);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -809,10 +821,10 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         const int ib = u + 1 + lane * NC, jb = u - dlo - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
-        BND2 = boundary2(cb + 1);
+        if (MODE == 1) BND2 = boundary2(cb + 1);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 1, MASKED>(H, E, F, CAP, S2, BND2, AmB2, lane, V2, k65536);
+      const int lmax = step16<NREG, 1, MODE>(H, E, F, CAP, S2, BND2, AmB2, lane, V2, k65536);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -878,9 +890,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 
   {
     const int head_end = min(cs, c_last + 1);                 // head: cb < cs (and cb <= c_last)
-    run_phase(TrueT{}, cb < head_end ? (head_end - cb + 1) >> 1 : 0);
-    run_phase(FalseT{}, cb + 1 <= ce ? ((ce - cb + 1) >> 1) : 0);  // steady: cb + 1 <= ce
-    run_phase(TrueT{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);  // tail: cb <= c_last
+    run_phase(Mode<1>{}, cb < head_end ? (head_end - cb + 1) >> 1 : 0);
+    run_phase(Mode<0>{}, cb + 1 <= ce ? ((ce - cb + 1) >> 1) : 0);  // steady: cb + 1 <= ce
+    run_phase(Mode<2>{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);  // tail: cb <= c_last
   }
   if (!stop) process16<NREG, 1, TRACE, false>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
   resolve_G16<NREG>(s, snap, lane);
