@@ -47,7 +47,7 @@ constexpr int kMaxChunks = 255;         // input chunks of one call (chunk ids a
 constexpr uint64_t kChunkBytes = 48ull << 20;  // target ASCII bytes per streamed chunk
 
 struct AlignArgs {
-  uint32_t* rw;              // packed R words, pair p starts at word (ref_off[p] >> 3) + p
+  uint32_t* rw;              // packed R words, pair p starts at word (ref_off[p] >> 3) + 2p
   uint32_t* qw;              // packed reversed-Q words, same addressing with qry_off
   const uint8_t* ref_ascii;  // ASCII inputs (device), packed by the align kernel (a1)
   const uint8_t* qry_ascii;
@@ -117,13 +117,15 @@ __device__ __forceinline__ uint32_t base_code(uint8_t ch, bool nmap, int* err) {
   return c;
 }
 
+// Word w of a packed sequence whose first base sits at nibble `pad` (0..7): nibble t
+// holds base 8w + t - pad (forward) or base len-1-(8w + t - pad) (reversed), 0 outside.
 __device__ __forceinline__ uint32_t pack_word(const uint8_t* seq, int64_t len, int64_t w, bool rev,
-                                              bool nmap, int* err) {
+                                              bool nmap, int* err, int pad = 0) {
   uint32_t word = 0;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
-    const int64_t k = 8 * w + t;
-    if (k < len) {
+    const int64_t k = 8 * w + t - pad;
+    if (k >= 0 && k < len) {
       const uint8_t ch = rev ? seq[len - 1 - k] : seq[k];
       word |= base_code(ch, nmap, err) << (4 * t);
     }
@@ -143,13 +145,13 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void pack_pair_fused(const uint8_t* __restrict__ ref, const uint8_t* __restrict__ qry,
                                                 uint64_t r0, uint64_t q0, int m, int n, uint32_t* Rw,
                                                 uint32_t* Qw, const int* ready, int chunk, bool nmap,
-                                                int* err_flags, int lane) {
+                                                int* err_flags, int lane, int padR = 0, int padQ = 0) {
   if (ready) {
     while (ld_acquire(ready + chunk) == 0) __nanosleep(500);
   }
   int err = 0;
-  for (int w = lane; w < (m + 7) / 8; w += 32) Rw[w] = pack_word(ref + r0, m, w, false, nmap, &err);
-  for (int w = lane; w < (n + 7) / 8; w += 32) Qw[w] = pack_word(qry + q0, n, w, true, nmap, &err);
+  for (int w = lane; w < (m + padR + 7) / 8; w += 32) Rw[w] = pack_word(ref + r0, m, w, false, nmap, &err, padR);
+  for (int w = lane; w < (n + padQ + 7) / 8; w += 32) Qw[w] = pack_word(qry + q0, n, w, true, nmap, &err, padQ);
   if (__any_sync(kFull, err) && lane == 0) atomicOr(err_flags, 1);
   __syncwarp();
 }
@@ -280,8 +282,8 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
     }
     return;
   }
-  uint32_t* Rw = A.rw + (r0 >> 3) + pid;
-  uint32_t* Qw = A.qw + (q0 >> 3) + pid;
+  uint32_t* Rw = A.rw + (r0 >> 3) + 2 * pid;
+  uint32_t* Qw = A.qw + (q0 >> 3) + 2 * pid;
   const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
   pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
                   A.nmap != 0, A.err_flags, lane);
@@ -680,14 +682,20 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     }
     return;
   }
-  uint32_t* Rw = A.rw + (r0 >> 3) + pid;
-  uint32_t* Qw = A.qw + (q0 >> 3) + pid;
-  const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
-  pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
-                  A.nmap != 0, A.err_flags, lane);
   const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;
   const int br = (A.br < 0 || A.br > m) ? m : A.br;
   const int alpha = A.alpha, beta = A.beta;
+  // Phase-aligned packing: R starts at nibble padR and Q (reversed) at nibble padQ so
+  // that every lane's R window offset starts at 0 and its Q offset at 7; both windows
+  // then advance one word together every 8 iterations (one refill point, not two).
+  const int u0 = ((2 - ((-bl) & 1)) + (-bl)) >> 1;
+  const int padR = (1 - u0) & 7;
+  const int padQ = (7 - (n - bl - u0)) & 7;
+  uint32_t* Rw = A.rw + (r0 >> 3) + 2 * pid;
+  uint32_t* Qw = A.qw + (q0 >> 3) + 2 * pid;
+  const int nwR = (m + padR + 7) >> 3, nwQ = (n + padQ + 7) >> 3;
+  pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
+                  A.nmap != 0, A.err_flags, lane, padR, padQ);
 
   State16 s;
   s.m = m; s.n = n; s.dlo = -bl; s.D = bl + br + 1; s.alpha = alpha; s.beta = beta;
@@ -735,12 +743,12 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     F[j] = W2;
   }
 
-  int rpos = u - 1 + lane * NC;
-  int wR = rpos >> 3, oR = rpos & 7;
+  int rpos = u - 1 + padR + lane * NC;
+  int wR = rpos >> 3, oR = rpos & 7;  // oR = 0
   uint32_t Wr0 = load_word_rw(Rw, wR, nwR), Wr1 = load_word_rw(Rw, wR + 1, nwR),
            Wr2 = load_word_rw(Rw, wR + 2, nwR), nR = load_word_rw(Rw, wR + 3, nwR);
-  int qpos = n + dlo - u + lane * NC;
-  int wQ = qpos >> 3, oQ = qpos & 7;
+  int qpos = n + dlo - u + padQ + lane * NC;
+  int wQ = qpos >> 3, oQ = qpos & 7;  // oQ = 7 = 7 - oR from here on
   uint32_t Wq0 = load_word_rw(Qw, wQ, nwQ), Wq1 = load_word_rw(Qw, wQ + 1, nwQ),
            Wq2 = load_word_rw(Qw, wQ + 2, nwQ), nQ = load_word_rw(Qw, wQ - 1, nwQ);
 
@@ -842,13 +850,11 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   // between runs of iterations whose count is computed up front, so the hot inner loop
   // carries no per-iteration refill predicates.
   auto housekeeping = [&]() {
-    if (oR == 8) {
+    if (oR == 8) {  // oQ == -1 at the same time (phase-aligned packing)
       oR = 0;
       ++wR;
       Wr0 = Wr1; Wr1 = Wr2; Wr2 = nR;
       nR = load_word_rw(Rw, wR + 3, nwR);
-    }
-    if (oQ < 0) {
       oQ = 7;
       --wQ;
       Wq2 = Wq1; Wq1 = Wq0; Wq0 = nQ;
@@ -874,7 +880,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   // run `total` iterations of one phase
   auto run_phase = [&](auto masked_tag, int total) {
     while (!stop && total > 0) {
-      int k = min(8 - oR, oQ + 1);
+      int k = 8 - oR;  // iters == oR (mod 8): runs end at refill / re-centring points together
       k = min(k, kRebase16 - iters);
       k = min(k, total);
       total -= k;
@@ -1219,7 +1225,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes64, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)P, 0, 40, st);
   if (sort_bytes64 > sort_bytes) sort_bytes = sort_bytes64;
-  if ((rc = grow(ctx->rw, 4 * (tot_r / 8 + P + 2))) || (rc = grow(ctx->qw, 4 * (tot_q / 8 + P + 2))) ||
+  if ((rc = grow(ctx->rw, 4 * (tot_r / 8 + 2 * P + 2))) || (rc = grow(ctx->qw, 4 * (tot_q / 8 + 2 * P + 2))) ||
       (rc = grow(ctx->nominal, 4 * P)) || (rc = grow(ctx->nominal_sorted, 4 * P)) ||
       (rc = grow(ctx->iota, 4 * P)) || (rc = grow(ctx->order, 4 * P)) || (rc = grow(ctx->bad, P)) ||
       (rc = grow(ctx->sort_tmp, sort_bytes)) || (rc = grow(ctx->scalars, 64)) ||
