@@ -33,15 +33,21 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in (SRC, HDR, __file__))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or stale():
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", SRC]
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile SRC into ``out``.  ``defines`` (e.g. ["AGATHA_FMA_ADD=0"]) build A/B
+    variants of the kernels for tools/ab_bench.sh; the default build uses none."""
+    if force or out != LIB or defines or stale():
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+               "-o", out + ".tmp", SRC]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = [a for a in sys.argv[1:] if a != "--force"]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    outs = [a[len("--out="):] for a in args if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose=True, out=outs[0] if outs else LIB, defines=defs))

@@ -47,7 +47,8 @@ constexpr int kMaxChunks = 255;         // input chunks of one call (chunk ids a
 constexpr uint64_t kChunkBytes = 48ull << 20;  // target ASCII bytes per streamed chunk
 
 struct AlignArgs {
-  uint32_t* rw;              // packed R words, pair p starts at word (ref_off[p] >> 3) + 2p
+  uint32_t* rw;              // packed R words, pair p's region starts at word (ref_off[p] >> 3) + 4p
+                             // (guard word, data, guard word: see load_word_rw)
   uint32_t* qw;              // packed reversed-Q words, same addressing with qry_off
   const uint8_t* ref_ascii;  // ASCII inputs (device), packed by the align kernel (a1)
   const uint8_t* qry_ascii;
@@ -73,6 +74,9 @@ struct AlignArgs {
   int sixteen;               // the constant 16, passed at run time (see make_key)
   uint32_t T16_0, T16_1;     // 16-bit kernel table: byte x = S + 2*alpha
   uint32_t k65536;           // the constant 65536, passed at run time (see shr16_fma)
+  uint32_t one;              // the constant 1, passed at run time (see add16x2_fma)
+  int ref16;                 // 16-bit kernel: stored value of the anti-diagonal max after
+                             // a re-centring (negative)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -82,12 +86,15 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 }
 
 // Code combination of eight cells at once (4-bit codes A0 C1 G2 T3 N4 in both R and
-// reversed Q): x = (r ^ q) | (r & q & 4) per nibble.  x == 0 exactly on a match of two
-// non-N bases, x in 1..3 on a mismatch of two non-N bases, x in 4..7 when either is N
-// (N vs N gives 4).  One LOP3.
+// reversed Q, 8 for a position outside the sequence): x = (r ^ q) | (r & q & 0xC) per
+// nibble.  x == 0 exactly on a match of two non-N bases, x in 1..3 on a mismatch of two
+// non-N bases, x in 4..7 when either is N (N vs N gives 4), and bit 3 set when either
+// position is outside its sequence (a PRMT selector nibble with bit 3 set returns the
+// sign byte of a table entry: 0 for the 16-bit table, whose entries are all >= 0).
+// One LOP3.
 __device__ __forceinline__ uint32_t combine(uint32_t r, uint32_t q) {
-  uint32_t x;  // LUT 0xBC = (a ^ b) | (a & b & c) with a = r, b = q, c = 0x44444444
-  asm("lop3.b32 %0, %1, %2, %3, 0xBC;" : "=r"(x) : "r"(r), "r"(q), "n"(0x44444444));
+  uint32_t x;  // LUT 0xBC = (a ^ b) | (a & b & c) with a = r, b = q, c = 0xCCCCCCCC
+  asm("lop3.b32 %0, %1, %2, %3, 0xBC;" : "=r"(x) : "r"(r), "r"(q), "n"(0xCCCCCCCC));
   return x;
 }
 
@@ -118,17 +125,22 @@ __device__ __forceinline__ uint32_t base_code(uint8_t ch, bool nmap, int* err) {
 }
 
 // Word w of a packed sequence whose first base sits at nibble `pad` (0..7): nibble t
-// holds base 8w + t - pad (forward) or base len-1-(8w + t - pad) (reversed), 0 outside.
+// holds base 8w + t - pad (forward) or base len-1-(8w + t - pad) (reversed), and `fill`
+// for a position outside the sequence (0 in agatha_pack4's layout, the out-of-range
+// code 8 in the align kernels' own buffers).
+constexpr uint32_t kOutWord = 0x88888888u;
 __device__ __forceinline__ uint32_t pack_word(const uint8_t* seq, int64_t len, int64_t w, bool rev,
-                                              bool nmap, int* err, int pad = 0) {
+                                              bool nmap, int* err, int pad = 0, uint32_t fill = 0) {
   uint32_t word = 0;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int64_t k = 8 * w + t - pad;
+    uint32_t c = fill;
     if (k >= 0 && k < len) {
       const uint8_t ch = rev ? seq[len - 1 - k] : seq[k];
-      word |= base_code(ch, nmap, err) << (4 * t);
+      c = base_code(ch, nmap, err);
     }
+    word |= c << (4 * t);
   }
   return word;
 }
@@ -150,20 +162,28 @@ __device__ __forceinline__ void pack_pair_fused(const uint8_t* __restrict__ ref,
     while (ld_acquire(ready + chunk) == 0) __nanosleep(500);
   }
   int err = 0;
-  for (int w = lane; w < (m + padR + 7) / 8; w += 32) Rw[w] = pack_word(ref + r0, m, w, false, nmap, &err, padR);
-  for (int w = lane; w < (n + padQ + 7) / 8; w += 32) Qw[w] = pack_word(qry + q0, n, w, true, nmap, &err, padQ);
+  const int nwR = (m + padR + 7) / 8, nwQ = (n + padQ + 7) / 8;
+  for (int w = lane; w < nwR; w += 32) Rw[1 + w] = pack_word(ref + r0, m, w, false, nmap, &err, padR, 8u);
+  for (int w = lane; w < nwQ; w += 32) Qw[1 + w] = pack_word(qry + q0, n, w, true, nmap, &err, padQ, 8u);
+  if (lane == 0) {
+    Rw[0] = kOutWord; Rw[nwR + 1] = kOutWord;
+    Qw[0] = kOutWord; Qw[nwQ + 1] = kOutWord;
+  }
   if (__any_sync(kFull, err) && lane == 0) atomicOr(err_flags, 1);
   __syncwarp();
 }
 
 // Packed words are written by this kernel (pack_pair_fused), so they are read with
 // plain loads, not through the read-only path.
+// A packed sequence occupies nw + 2 words from `base`: a guard word (kOutWord), data
+// words 0..nw-1 at base[1..nw], another guard.  Clamping w + 1 to [0, nw + 1] returns
+// the out-of-range code for every position outside the sequence.
 __device__ __forceinline__ uint32_t load_word_rw(const uint32_t* base, int w, int nw) {
-  w = w < 0 ? 0 : (w >= nw ? nw - 1 : w);
-  return base[w];
+  int i = w + 1;
+  i = i < 0 ? 0 : (i > nw + 1 ? nw + 1 : i);
+  return base[i];
 }
 
-template <int M> struct Mode { static constexpr int value = M; };
 struct TrueT { static constexpr bool value = true; };
 struct FalseT { static constexpr bool value = false; };
 
@@ -282,8 +302,8 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
     }
     return;
   }
-  uint32_t* Rw = A.rw + (r0 >> 3) + 2 * pid;
-  uint32_t* Qw = A.qw + (q0 >> 3) + 2 * pid;
+  uint32_t* Rw = A.rw + (r0 >> 3) + 4 * pid;
+  uint32_t* Qw = A.qw + (q0 >> 3) + 4 * pid;
   const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
   pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
                   A.nmap != 0, A.err_flags, lane);
@@ -329,11 +349,11 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
   int rpos = u - 1 + lane * (K / 2);          // nibble index of R[i] at t = 0, PAR = 0
   int wR = rpos >> 3, oR = rpos & 7;
   uint32_t Wr0 = load_word_rw(Rw, wR, nwR), Wr1 = load_word_rw(Rw, wR + 1, nwR),
-           Wr2 = load_word_rw(Rw, wR + 2, nwR), nR = load_word_rw(Rw, wR + 3, nwR);
+           Wr2 = load_word_rw(Rw, wR + 2, nwR);
   int qpos = n + dlo - u + lane * (K / 2);    // nibble index of Qrev[x] at t = 0
   int wQ = qpos >> 3, oQ = qpos & 7;
   uint32_t Wq0 = load_word_rw(Qw, wQ, nwQ), Wq1 = load_word_rw(Qw, wQ + 1, nwQ),
-           Wq2 = load_word_rw(Qw, wQ + 2, nwQ), nQ = load_word_rw(Qw, wQ - 1, nwQ);
+           Wq2 = load_word_rw(Qw, wQ + 2, nwQ);
 
   const uint32_t T0 = A.T0, T1 = A.T1;
   int lk_prev = kNegKey, rH_prev = kEmptyH - 1;  // nothing pending before the first step
@@ -392,14 +412,12 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
     if (++oR == 8) {
       oR = 0;
       ++wR;
-      Wr0 = Wr1; Wr1 = Wr2; Wr2 = nR;
-      nR = load_word_rw(Rw, wR + 3, nwR);
+      Wr0 = Wr1; Wr1 = Wr2; Wr2 = load_word_rw(Rw, wR + 2, nwR);
     }
     if (--oQ < 0) {
       oQ = 7;
       --wQ;
-      Wq2 = Wq1; Wq1 = Wq0; Wq0 = nQ;
-      nQ = load_word_rw(Qw, wQ - 1, nwQ);
+      Wq2 = Wq1; Wq1 = Wq0; Wq0 = load_word_rw(Qw, wQ, nwQ);
     }
   };
 
@@ -473,9 +491,13 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignAr
 // every live value stays in (-16000, 12000) and no half-word add wraps.
 // ===================================================================================
 
-constexpr int kW16 = -28000;       // "-infinity" (walls, E/F of boundary cells)
-constexpr int kCapNeg16 = -20000;  // padding cap
-constexpr int kEmpty16 = -16000;   // lane max at or below: no valid cell on the anti-diagonal
+#ifndef AGATHA_FMA_ADD
+#define AGATHA_FMA_ADD 1
+#endif
+constexpr int kW16 = -29250;       // "-infinity" (walls, E/F of boundary cells)
+constexpr int kCapNeg16 = -21250;  // padding cap
+constexpr int kEmpty16 = -17250;   // lane max at or below: no valid cell on the anti-diagonal
+constexpr int kTop16 = -129;       // every stored H is at most this
 constexpr int kRebase16 = 32;      // iterations (64 anti-diagonals) between re-centrings
 
 __device__ __forceinline__ uint32_t pack2(int lo, int hi) {
@@ -498,6 +520,14 @@ __device__ __forceinline__ int hi16_fma(uint32_t x, uint32_t k65536) {
   return d;
 }
 __device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vmins2(a, b); }
+// Half-word pair add h + s on the FMA pipe (IMAD h * one + s).  Exact with no carry
+// between the halves because every stored H half is in [-32768, kTop16] and every
+// s half in [0, 127]: each low-half sum stays negative, so it never wraps past 0xFFFF.
+__device__ __forceinline__ uint32_t add16x2_fma(uint32_t h, uint32_t s, uint32_t one) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(h), "r"(one), "r"(s));
+  return d;
+}
 __device__ __forceinline__ uint32_t vaddmax2(uint32_t a, uint32_t b, uint32_t c) {
   return __viaddmax_s16x2(a, b, c);
 }
@@ -608,15 +638,16 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
 
 // One anti-diagonal step on the NREG/2 registers of parity PAR.  S2[k] holds the
 // shifted substitution scores (S + 2alpha) of register PAR+2k as a half-word pair.
-// MODE 0: steady (every band slot in the table); 1: head (cells before the table hold
-// the boundary value, E/F = -infinity, and are excluded from the max); 2: tail (cells
-// past the table end are never read by a valid cell, so they are only excluded from
-// the max).
-template <int NREG, int PAR, int MODE>
+// MASKED (head and tail anti-diagonals): cells outside the table are computed like the
+// others and only excluded from the max (Eq. 5).  Their substitution score is 0 (the
+// out-of-range nibble code, see combine), which makes every cell before the table hold
+// exactly the boundary value of reading R2 with E/F at most H - (alpha - beta), so the
+// cells a valid cell reads are exact without any select ("Masking").
+template <int NREG, int PAR, bool MASKED>
 __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], uint32_t (&F)[NREG],
                                       const uint32_t (&CAP)[NREG], const uint32_t (&S2)[NREG / 2],
-                                      uint32_t BND2, uint32_t AmB2, int lane, uint32_t V2,
-                                      uint32_t k65536) {
+                                      uint32_t AmB2, int lane, uint32_t V2, uint32_t k65536,
+                                      uint32_t one) {
   const uint32_t W2 = pack2(kW16, kW16);
   uint32_t xH, xEF;
   if (PAR == 0) {  // register 0: (lane-1's slot K-1, own slot NREG-1) from register NREG-1
@@ -642,25 +673,19 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
     const uint32_t fl = (j == NREG - 1) ? xEF : F[j + 1];
     const uint32_t e = vaddmax2(eu, AmB2, hu);                 // Eq. 2 (shifted)
     const uint32_t f = vaddmax2(fl, AmB2, hl);                 // Eq. 3 (shifted)
-    uint32_t h = vaddmax2(H[j], S2[k], vmax2(e, f));           // Eq. 1 (shifted)
-    h = vmin2(h, CAP[j]);                                      // padding slots stay <= -20000
-    if (MODE == 1) {
+#if AGATHA_FMA_ADD
+    uint32_t h = __vimax3_s16x2(add16x2_fma(H[j], S2[k], one), e, f);  // Eq. 1 (shifted)
+#else
+    uint32_t h = vaddmax2(H[j], S2[k], vmax2(e, f));                    // Eq. 1 (shifted)
+#endif
+    h = vmin2(h, CAP[j]);                                      // padding slots stay <= kCapNeg16
+    H[j] = h;
+    E[j] = e;
+    F[j] = f;
+    if (MASKED) {
       // V2 bit k: cell t = k in the table; bit 16+k: cell t = k + NREG/2 in the table
       const uint32_t M = ((V2 >> k) & 0x00010001u) * 0xFFFFu;
-      H[j] = (h & M) | (BND2 & ~M);
-      E[j] = (e & M) | (W2 & ~M);
-      F[j] = (f & M) | (W2 & ~M);
       h = (h & M) | (W2 & ~M);
-    } else if (MODE == 2) {
-      const uint32_t M = ((V2 >> k) & 0x00010001u) * 0xFFFFu;
-      H[j] = h;
-      E[j] = e;
-      F[j] = f;
-      h = (h & M) | (W2 & ~M);
-    } else {
-      H[j] = h;
-      E[j] = e;
-      F[j] = f;
     }
     if (k & 1) lm = __vimax3_s16x2(lm, prev, h); else prev = h;  // Eq. 5, per half
   }
@@ -688,11 +713,11 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   // Phase-aligned packing: R starts at nibble padR and Q (reversed) at nibble padQ so
   // that every lane's R window offset starts at 0 and its Q offset at 7; both windows
   // then advance one word together every 8 iterations (one refill point, not two).
-  const int u0 = ((2 - ((-bl) & 1)) + (-bl)) >> 1;
+  const int u0 = (((-bl) & 1) + (-bl)) >> 1;  // u of the first step (cb = dlo mod 2, below)
   const int padR = (1 - u0) & 7;
   const int padQ = (7 - (n - bl - u0)) & 7;
-  uint32_t* Rw = A.rw + (r0 >> 3) + 2 * pid;
-  uint32_t* Qw = A.qw + (q0 >> 3) + 2 * pid;
+  uint32_t* Rw = A.rw + (r0 >> 3) + 4 * pid;
+  uint32_t* Qw = A.qw + (q0 >> 3) + 4 * pid;
   const int nwR = (m + padR + 7) >> 3, nwQ = (n + padQ + 7) >> 3;
   pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
                   A.nmap != 0, A.err_flags, lane, padR, padQ);
@@ -700,7 +725,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   State16 s;
   s.m = m; s.n = n; s.dlo = -bl; s.D = bl + br + 1; s.alpha = alpha; s.beta = beta;
   s.mn = (A.variant & AGATHA_VAR_CHECK_LAST) ? m + n + 1 : m + n;  // Eq. 4 tested for c < mn
-  s.zdrop = A.zdrop; s.B = 0; s.posValid = true;
+  s.zdrop = A.zdrop; s.B = -A.ref16; s.posValid = true;  // stored = X + alpha*c + ref16
   s.G_H = INT_MIN / 2; s.G_c = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.zthr = INT_MIN;
   if (A.variant & AGATHA_VAR_ORIGIN_MAX) {  // G = H(0,0) = 0 at the origin
     s.G_H = 0;
@@ -717,13 +742,18 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   const int dmid = min(max(m - n, dlo), dhi);
   const int c_last = fdiag(dmid);
 
-  int cb = 2 - (dlo & 1);
+  // The first step computes anti-diagonal cb = 0 (even dlo) or 1 (odd dlo): the origin
+  // and the first boundary cells come out of the DP itself, which starts the two gap
+  // chains along the boundary (E of (i,0), F of (0,j)) that the masked steps carry.
+  int cb = dlo & 1;
   int u = (cb + dlo) >> 1;
   // boundary value of diagonal d (reading R2); slots beyond the band hold the cap
   auto bnd = [&](int d) { const int ad = d < 0 ? -d : d; return d == 0 ? 0 : -(alpha + (ad - 1) * beta); };
 
   // a3: slot k of register j (j or j+NREG) on diagonal dlo + K*lane + k; a slot of
-  // parity(cb) holds anti-diagonal cb-2, the other parity cb-1 (B = 0).
+  // parity(cb) holds anti-diagonal cb-2, the other parity cb-1 (both <= 0).  Slots start
+  // at bnd(d) + alpha*c (stored units), diagonal 0 at the origin value 0, E/F at -inf;
+  // DESIGN.md §6.2 "Masking" shows these reproduce the boundary exactly.
   uint32_t H[NREG], E[NREG], F[NREG], CAP[NREG];
   const uint32_t W2 = pack2(kW16, kW16);
 #pragma unroll
@@ -735,7 +765,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       const bool valid = g < D;
       c2[h] = valid ? 32767 : kCapNeg16;
       const int ci = ((k & 1) == 0) ? cb - 2 : cb - 1;  // (dlo + K*lane) has parity of cb
-      v2[h] = valid ? bnd(d) + alpha * ci : kCapNeg16;
+      v2[h] = valid ? (d == 0 ? 0 : bnd(d) + alpha * ci) - s.B : kCapNeg16;
     }
     H[j] = pack2(v2[0], v2[1]);
     CAP[j] = pack2(c2[0], c2[1]);
@@ -746,14 +776,15 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   int rpos = u - 1 + padR + lane * NC;
   int wR = rpos >> 3, oR = rpos & 7;  // oR = 0
   uint32_t Wr0 = load_word_rw(Rw, wR, nwR), Wr1 = load_word_rw(Rw, wR + 1, nwR),
-           Wr2 = load_word_rw(Rw, wR + 2, nwR), nR = load_word_rw(Rw, wR + 3, nwR);
+           Wr2 = load_word_rw(Rw, wR + 2, nwR);
   int qpos = n + dlo - u + padQ + lane * NC;
   int wQ = qpos >> 3, oQ = qpos & 7;  // oQ = 7 = 7 - oR from here on
   uint32_t Wq0 = load_word_rw(Qw, wQ, nwQ), Wq1 = load_word_rw(Qw, wQ + 1, nwQ),
-           Wq2 = load_word_rw(Qw, wQ + 2, nwQ), nQ = load_word_rw(Qw, wQ - 1, nwQ);
+           Wq2 = load_word_rw(Qw, wQ + 2, nwQ);
 
-  const uint32_t T0 = A.T16_0, T1 = A.T16_1, k65536 = A.k65536;
-  int rH_prev = kEmpty16 - 1, B_prev = 0, tlo_prev = 0, thi_prev = NC - 1;
+  const uint32_t T0 = A.T16_0, T1 = A.T16_1, k65536 = A.k65536, one = A.one;
+  const int ref16 = -s.B;
+  int rH_prev = kEmpty16 - 1, B_prev = s.B, tlo_prev = 0, thi_prev = NC - 1;
   bool stop = false;
   int iters = 0;
 
@@ -779,14 +810,6 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
     }
   };
-  // Masked steps: the held value of a cell outside the table.  Only boundary cells
-  // (i = 0 or j = 0) are ever read, and on anti-diagonal c both have the value
-  // H = -(alpha + (c-1) beta) (reading R2), so one broadcast value serves every slot.
-  auto boundary2 = [&](int c) {
-    int v = (c == 0 ? 0 : -(alpha + (c - 1) * beta)) + alpha * c - s.B;
-    v = min(max(v, -30000), 30000);
-    return pack2(v, v);
-  };
   // bit t (t < NC/2) and bit 16 + t - NC/2 (t >= NC/2) set for the cells t in [tlo, thi]
   auto valid_bits = [&](int tlo, int thi) {
     const int lo = max(tlo, 0), hi = min(thi, NC - 1);
@@ -795,10 +818,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     return (v & ((1u << (NC / 2)) - 1u)) | ((v >> (NC / 2)) << 16);
   };
 
-  auto iteration = [&](auto mode_tag) {
-    constexpr int MODE = decltype(mode_tag)::value;
-    constexpr bool MASKED = MODE != 0;
-    uint32_t qg[2], S2[NREG / 2], BND2 = 0u, V2 = 0u;
+  auto iteration = [&](auto masked_tag) {
+    constexpr bool MASKED = decltype(masked_tag)::value;
+    uint32_t qg[2], S2[NREG / 2], V2 = 0u;
     const uint32_t Wq[3] = {Wq0, Wq1, Wq2}, Wr[3] = {Wr0, Wr1, Wr2};
     qg[0] = __funnelshift_rc(Wq[0], Wq[1], 4 * oQ);
     qg[1] = __funnelshift_rc(Wq[1], Wq[2], 4 * oQ);
@@ -810,10 +832,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         const int ib = u + lane * NC, jb = u - dlo - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
-        if (MODE == 1) BND2 = boundary2(cb);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 0, MODE>(H, E, F, CAP, S2, BND2, AmB2, lane, V2, k65536);
+      const int lmax = step16<NREG, 0, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -829,10 +850,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         const int ib = u + 1 + lane * NC, jb = u - dlo - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
-        if (MODE == 1) BND2 = boundary2(cb + 1);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 1, MODE>(H, E, F, CAP, S2, BND2, AmB2, lane, V2, k65536);
+      const int lmax = step16<NREG, 1, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -853,17 +873,15 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     if (oR == 8) {  // oQ == -1 at the same time (phase-aligned packing)
       oR = 0;
       ++wR;
-      Wr0 = Wr1; Wr1 = Wr2; Wr2 = nR;
-      nR = load_word_rw(Rw, wR + 3, nwR);
+      Wr0 = Wr1; Wr1 = Wr2; Wr2 = load_word_rw(Rw, wR + 2, nwR);
       oQ = 7;
       --wQ;
-      Wq2 = Wq1; Wq1 = Wq0; Wq0 = nQ;
-      nQ = load_word_rw(Qw, wQ - 1, nwQ);
+      Wq2 = Wq1; Wq1 = Wq0; Wq0 = load_word_rw(Qw, wQ, nwQ);
     }
-    if (iters >= kRebase16) {  // re-centre the base on the last anti-diagonal max
+    if (iters >= kRebase16) {  // re-centre: the last anti-diagonal max moves to ref16
       iters = 0;
       if (rH_prev > kEmpty16) {
-        const int delta = rH_prev + B_prev - s.B;
+        const int delta = rH_prev + B_prev - s.B - ref16;
         const uint32_t nd2 = pack2(-delta, -delta);
 #pragma unroll
         for (int j = 0; j < NREG; ++j) {
@@ -896,9 +914,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 
   {
     const int head_end = min(cs, c_last + 1);                 // head: cb < cs (and cb <= c_last)
-    run_phase(Mode<1>{}, cb < head_end ? (head_end - cb + 1) >> 1 : 0);
-    run_phase(Mode<0>{}, cb + 1 <= ce ? ((ce - cb + 1) >> 1) : 0);  // steady: cb + 1 <= ce
-    run_phase(Mode<2>{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);  // tail: cb <= c_last
+    run_phase(TrueT{}, cb < head_end ? (head_end - cb + 1) >> 1 : 0);
+    run_phase(FalseT{}, cb + 1 <= ce ? ((ce - cb + 1) >> 1) : 0);  // steady: cb + 1 <= ce
+    run_phase(TrueT{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);  // tail: cb <= c_last
   }
   if (!stop) process16<NREG, 1, TRACE, false>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
   resolve_G16<NREG>(s, snap, lane);
@@ -1098,13 +1116,31 @@ void score_table(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
 // 16-bit packed kernel eligibility: the within-anti-
 // diagonal spread of H plus the drift between re-centrings must stay inside the
 // half-word range with margin, and S + 2*alpha must fit the int8 score table.
+// the anti-diagonal max sits at ref16 after a re-centring; every stored H
+// stays in (kEmpty16, kTop16] and every wall/cap value above -32768.
+static long long drift16(const agatha_params_t* p) {
+  const long long mx = std::max<long long>(p->match, std::max<long long>(p->mismatch, p->ambig));
+  return 70 * (2 * (long long)p->gap_open + mx);
+}
+// Cells outside the table may rise above the anti-diagonal max of the valid cells by at
+// most (alpha - beta) per anti-diagonal for as long as they stay outside (at most
+// maxD + 2 anti-diagonals); the ref16 margin covers that, the drift between
+// re-centrings and the largest table entry, so every stored H stays <= kTop16.
+static int ref16_of(const agatha_params_t* p, int maxD) {
+  const long long a = p->match, al = p->gap_open, be = p->gap_extend;
+  const long long mx = std::max<long long>(a, std::max<long long>(p->mismatch, p->ambig));
+  return (int)(kTop16 - 127 - (drift16(p) + 3 * al + 2 * a + mx + (al - be) * ((long long)maxD + 2)));
+}
 bool use16(const agatha_params_t* p, int maxD) {
   const long long a = p->match, al = p->gap_open, be = p->gap_extend;
   const long long mx = std::max<long long>(a, std::max<long long>(p->mismatch, p->ambig));
   const long long spread = al + (long long)maxD * (be + a + mx) + 4 * mx;
-  const long long drift = 70 * (2 * al + mx);
-  if (a + 2 * al > 127 || 2 * al - mx < -128) return false;
-  return spread + drift < 15000 && drift + al + a + 127 < 12000 && maxD <= kMaxSlots;
+  const long long drift = drift16(p);
+  // int8 table entries S + 2*alpha must lie in [0, 127] (add16x2_fma); alpha >= beta
+  // (the boundary chains of the masked steps)
+  if (a + 2 * al > 127 || 2 * al - p->mismatch < 0 || 2 * al - p->ambig < 0 || al < be) return false;
+  const long long ref = ref16_of(p, maxD);
+  return ref - (spread + drift) > kEmpty16 && kW16 - drift > -32768 && maxD <= kMaxSlots;
 }
 
 void score_table16(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
@@ -1225,7 +1261,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes64, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)P, 0, 40, st);
   if (sort_bytes64 > sort_bytes) sort_bytes = sort_bytes64;
-  if ((rc = grow(ctx->rw, 4 * (tot_r / 8 + 2 * P + 2))) || (rc = grow(ctx->qw, 4 * (tot_q / 8 + 2 * P + 2))) ||
+  if ((rc = grow(ctx->rw, 4 * (tot_r / 8 + 4 * P + 4))) || (rc = grow(ctx->qw, 4 * (tot_q / 8 + 4 * P + 4))) ||
       (rc = grow(ctx->nominal, 4 * P)) || (rc = grow(ctx->nominal_sorted, 4 * P)) ||
       (rc = grow(ctx->iota, 4 * P)) || (rc = grow(ctx->order, 4 * P)) || (rc = grow(ctx->bad, P)) ||
       (rc = grow(ctx->sort_tmp, sort_bytes)) || (rc = grow(ctx->scalars, 64)) ||
@@ -1290,6 +1326,8 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   A.alpha = p->gap_open; A.beta = p->gap_extend; A.zdrop = p->zdrop; A.sixteen = 16;
   A.variant = p->variant;
   A.k65536 = 65536u;
+  A.one = 1u;
+  A.ref16 = ref16_of(p, maxD);
   score_table(p, &A.T0, &A.T1);
   score_table16(p, &A.T16_0, &A.T16_1);
   A.trace_pair = trace_pair; A.trace_score = trace_score; A.trace_i = trace_i; A.trace_cap = trace_cap;

@@ -84,9 +84,15 @@ def test_scoring_near_the_guard(gpu_lib, ctx):
                 q[k] = "ACGT"[int(rng.integers(0, 4))]
         lst.append((a, "".join(q) + rand_seq(rng, 500)))
     pairs = synth.from_list(lst)
-    # alpha + D*(beta + a + max(b,n)) + 4*max + 70*(2*alpha + max) just under 15000 at w=300
+    # DESIGN.md §6.2 guard: ref16 - (spread + drift) > -17250 with
+    #   spread = alpha + D*(beta + a + max(b,n)) + 4*max, drift = 70*(2*alpha + max),
+    #   ref16 = -256 - (drift + 3*alpha + 2*a + max + (alpha - beta)*(D + 2));
+    # at w = 280 (D = 561) this is -17040: 210 inside the limit
     both(gpu_lib, ctx, pairs, dict(match=5, mismatch=9, ambig=9, gap_open=9, gap_extend=4,
-                                   band_left=300, band_right=300, zdrop=-1), expect16=True)
+                                   band_left=280, band_right=280, zdrop=-1), expect16=True)
+    # w = 290: -17500, just outside: the 32-bit kernel runs
+    both(gpu_lib, ctx, pairs, dict(match=5, mismatch=9, ambig=9, gap_open=9, gap_extend=4,
+                                   band_left=290, band_right=290, zdrop=-1), expect16=False)
     both(gpu_lib, ctx, pairs, dict(match=3, mismatch=12, ambig=2, gap_open=30, gap_extend=1,
                                    band_left=200, band_right=250, zdrop=200))
     both(gpu_lib, ctx, pairs, dict(match=12, mismatch=12, ambig=12, gap_open=12, gap_extend=6,
