@@ -37,13 +37,13 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-# DESIGN.md §6.1 "Roofline": the path is ALU-pipe bound.  Algorithmic work per cell =
+# DESIGN.md §6.3 "Roofline": the path is ALU-pipe bound.  Algorithmic work per cell =
 # the minimal ALU-pipe lane-instruction count on sm_100a with DPX .S16x2 (two cells per
-# lane-instruction): Eq. 2 0.5 + Eq. 3 0.5 + Eq. 1 1.0 (max + fused add/max) + S lookup
-# 0.5 + Eq. 5 running max 0.25 = 2.75.  Peak = 148 SMs x 64 ALU lanes/clk (4 SMSP x 16,
+# lane-instruction) and the Eq. 1 add on the FMA pipe: Eq. 2 0.5 + Eq. 3 0.5 + Eq. 1 0.5
+# (3-input max) + S lookup 0.5 + Eq. 5 running max 0.25 = 2.25.  Peak = 148 SMs x 64 ALU lanes/clk (4 SMSP x 16,
 # B300_MICROARCH "alu-pipe rt_SMSP=2"; measured 62.4-62.5, profiles/r01_dpx16.jsonl) x
 # clocks.max.sm.
-OPS_PER_CELL = 2.75
+OPS_PER_CELL = 2.25
 SM_COUNT = 148
 LANES_PER_CLK_PER_SM = 64
 # dram__bytes_read.sum + dram__bytes_write.sum per align launch on the full C2 batch, from
