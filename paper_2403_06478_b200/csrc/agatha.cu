@@ -690,7 +690,10 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
     if (k & 1) lm = __vimax3_s16x2(lm, prev, h); else prev = h;  // Eq. 5, per half
   }
   if ((NREG / 2) & 1) lm = vmax2(lm, prev);
-  return max(lo16(lm), hi16_fma(lm, k65536));
+  // max of the two halves as an int32: hi16_fma gives (sign(hi) = -1 : hi), and every
+  // H half is negative (<= kTop16), so the pair max is (-1 : max(lo, hi)), which read as
+  // an int32 is exactly max(lo, hi)
+  return (int)vmax2(lm, (uint32_t)hi16_fma(lm, k65536));
 }
 
 template <int NREG, bool TRACE>
@@ -880,6 +883,8 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     }
     if (iters >= kRebase16) {  // re-centre: the last anti-diagonal max moves to ref16
       iters = 0;
+      // (only the last 1-2 anti-diagonals of a pair can be empty with D >= 2; a
+      // one-diagonal band, where every other one is empty, runs the 32-bit kernel)
       if (rH_prev > kEmpty16) {
         const int delta = rH_prev + B_prev - s.B - ref16;
         const uint32_t nd2 = pack2(-delta, -delta);
@@ -1139,6 +1144,9 @@ bool use16(const agatha_params_t* p, int maxD) {
   // int8 table entries S + 2*alpha must lie in [0, 127] (add16x2_fma); alpha >= beta
   // (the boundary chains of the masked steps)
   if (a + 2 * al > 127 || 2 * al - p->mismatch < 0 || 2 * al - p->ambig < 0 || al < be) return false;
+  // a one-diagonal band (bl = br = 0) leaves every other anti-diagonal empty, so the
+  // re-centring (on the last anti-diagonal's max) would never run
+  if (p->band_left == 0 && p->band_right == 0) return false;
   const long long ref = ref16_of(p, maxD);
   return ref - (spread + drift) > kEmpty16 && kW16 - drift > -32768 && maxD <= kMaxSlots;
 }

@@ -124,3 +124,23 @@ def test_very_unequal_lengths(gpu_lib, ctx):
     for bl, br in [(500, 500), (511, 100), (100, 511), (0, 511)]:
         both(gpu_lib, ctx, pairs, dict(match=2, mismatch=4, ambig=4, gap_open=4, gap_extend=2,
                                        band_left=bl, band_right=br, zdrop=400))
+
+
+def test_narrow_bands_long_pairs(gpu_lib, ctx):
+    """Bands of 0-2 diagonals over long, near-identical pairs: scores climb by up to
+    (a + 2 alpha)/2 per anti-diagonal for thousands of anti-diagonals, so the base
+    re-centring must keep up (with bl = br = 0 every other anti-diagonal is empty and the
+    32-bit kernel runs)."""
+    rng = np.random.default_rng(26)
+    lst = []
+    for _ in range(6):
+        a = rand_seq(rng, int(rng.integers(6000, 9000)))
+        q = list(a)
+        for k in range(0, len(q), 997):
+            q[k] = "ACGT"[int(rng.integers(0, 4))]
+        lst.append((a, "".join(q)))
+    lst.append(("A" * 9000, "A" * 9000))
+    pairs = synth.from_list(lst)
+    for bl, br, exp16 in [(0, 0, False), (1, 0, True), (0, 1, True), (1, 1, True), (2, 2, True)]:
+        both(gpu_lib, ctx, pairs, dict(match=2, mismatch=4, ambig=4, gap_open=4, gap_extend=2,
+                                       band_left=bl, band_right=br, zdrop=-1), expect16=exp16)
