@@ -590,12 +590,13 @@ template <int NREG, int PARC, bool TRACE, bool STEADY>
 __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c, int rH, int Bc,
                                           int tlo, int thi, const uint32_t (&H)[NREG], int lane,
                                           uint32_t* snap, long long pid) {
-  // empty anti-diagonals are skipped (R11); with a one-diagonal band every other
-  // anti-diagonal is empty even in the steady phase, so this is always tested
-  const bool nonempty = rH > kEmpty16;
+  // Empty anti-diagonals are skipped (R11).  Inside the steady phase (STEADY: the
+  // anti-diagonal and the one before it lie inside the table, D >= 2) no anti-diagonal
+  // is empty and c < m + n, so the fast path is two compares.
+  const bool nonempty = (STEADY && !TRACE) || rH > kEmpty16;
   const int Hs = rH + Bc - s.alpha * c;
   const bool upd = nonempty && Hs > s.G_H;
-  const bool chk = nonempty && Hs < s.zthr && c < s.mn;
+  const bool chk = nonempty && Hs < s.zthr && ((STEADY && !TRACE) || c < s.mn);
   if (!__any_sync(kFull, upd || chk || (TRACE && nonempty))) return false;
   if (TRACE || chk) {
     uint32_t r[NREG / 2];
@@ -643,11 +644,17 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
 // out-of-range nibble code, see combine), which makes every cell before the table hold
 // exactly the boundary value of reading R2 with E/F at most H - (alpha - beta), so the
 // cells a valid cell reads are exact without any select ("Masking").
-template <int NREG, int PAR, bool MASKED>
+//
+// Band walls (DESIGN.md §6.1 "Layout"): the band's low end sits at lane 0 slot `off`;
+// the `off` slots under it are padding that the caps of registers < NCAP hold at
+// kCapNeg16.  Its high end is NREG-aligned, so the wall there is a half-word of the
+// PAR = 1 exchange (KEEPX clears it to -inf in the one lane that needs it), and the slots
+// above it are never read by a band cell; LMK removes them from the lane max.
+template <int NREG, int NCAP, int PAR, bool MASKED>
 __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], uint32_t (&F)[NREG],
-                                      const uint32_t (&CAP)[NREG], const uint32_t (&S2)[NREG / 2],
+                                      const uint32_t (&CAP)[NCAP], const uint32_t (&S2)[NREG / 2],
                                       uint32_t AmB2, int lane, uint32_t V2, uint32_t k65536,
-                                      uint32_t one) {
+                                      uint32_t one, uint32_t KEEPX, uint32_t LMK) {
   const uint32_t W2 = pack2(kW16, kW16);
   uint32_t xH, xEF;
   if (PAR == 0) {  // register 0: (lane-1's slot K-1, own slot NREG-1) from register NREG-1
@@ -657,11 +664,10 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
     xH = prmt(sh, H[NREG - 1], 0x5432);
     xEF = prmt(se, E[NREG - 1], 0x5432);
   } else {         // register NREG-1: (own slot NREG, lane+1's slot 0) from register 0
-    uint32_t sh = __shfl_down_sync(kFull, H[0], 1);
-    uint32_t sf = __shfl_down_sync(kFull, F[0], 1);
-    if (lane == 31) { sh = W2; sf = W2; }
-    xH = prmt(H[0], sh, 0x5432);
-    xEF = prmt(F[0], sf, 0x5432);
+    const uint32_t sh = __shfl_down_sync(kFull, H[0], 1);
+    const uint32_t sf = __shfl_down_sync(kFull, F[0], 1);
+    xH = (prmt(H[0], sh, 0x5432) & KEEPX) | (W2 & ~KEEPX);
+    xEF = (prmt(F[0], sf, 0x5432) & KEEPX) | (W2 & ~KEEPX);
   }
   uint32_t lm = W2, prev = W2;
 #pragma unroll
@@ -678,7 +684,7 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
 #else
     uint32_t h = vaddmax2(H[j], S2[k], vmax2(e, f));                    // Eq. 1 (shifted)
 #endif
-    h = vmin2(h, CAP[j]);                                      // padding slots stay <= kCapNeg16
+    if (j < NCAP) h = vmin2(h, CAP[j < NCAP ? j : 0]);         // padding slots stay <= kCapNeg16
     H[j] = h;
     E[j] = e;
     F[j] = f;
@@ -690,13 +696,14 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
     if (k & 1) lm = __vimax3_s16x2(lm, prev, h); else prev = h;  // Eq. 5, per half
   }
   if ((NREG / 2) & 1) lm = vmax2(lm, prev);
+  lm = (lm & LMK) | (W2 & ~LMK);  // slots above the band's high wall
   // max of the two halves as an int32: hi16_fma gives (sign(hi) = -1 : hi), and every
   // H half is negative (<= kTop16), so the pair max is (-1 : max(lo, hi)), which read as
   // an int32 is exactly max(lo, hi)
   return (int)vmax2(lm, (uint32_t)hi16_fma(lm, k65536));
 }
 
-template <int NREG, bool TRACE>
+template <int NREG, bool TRACE, int NCAP>
 __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap) {
   constexpr int K = 2 * NREG;        // slots per lane
   constexpr int NC = NREG;           // cells per step per lane (K/2)
@@ -713,12 +720,19 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;
   const int br = (A.br < 0 || A.br > m) ? m : A.br;
   const int alpha = A.alpha, beta = A.beta;
+  // Slot layout: slot g (lane g / K, slot g % K) holds diagonal dls + g.  The band
+  // [dlo, dhi] occupies slots [off, off + D) with off = (-D) mod NREG, so its high end
+  // off + D falls on a half-word boundary (a cheap wall) and the low padding fits in the
+  // first `off` <= NCAP registers of lane 0 (the capped ones).
+  const int Dband = bl + br + 1;
+  const int off = (int)__reduce_max_sync(kFull, (unsigned)((-Dband) & (NREG - 1)));
+  const int dls = -bl - off;
   // Phase-aligned packing: R starts at nibble padR and Q (reversed) at nibble padQ so
   // that every lane's R window offset starts at 0 and its Q offset at 7; both windows
   // then advance one word together every 8 iterations (one refill point, not two).
-  const int u0 = (((-bl) & 1) + (-bl)) >> 1;  // u of the first step (cb = dlo mod 2, below)
+  const int u0 = ((dls & 1) + dls) >> 1;  // u of the first step (cb = dls mod 2, below)
   const int padR = (1 - u0) & 7;
-  const int padQ = (7 - (n - bl - u0)) & 7;
+  const int padQ = (7 - (n + dls - u0)) & 7;
   uint32_t* Rw = A.rw + (r0 >> 3) + 4 * pid;
   uint32_t* Qw = A.qw + (q0 >> 3) + 4 * pid;
   const int nwR = (m + padR + 7) >> 3, nwQ = (n + padQ + 7) >> 3;
@@ -726,7 +740,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
                   A.nmap != 0, A.err_flags, lane, padR, padQ);
 
   State16 s;
-  s.m = m; s.n = n; s.dlo = -bl; s.D = bl + br + 1; s.alpha = alpha; s.beta = beta;
+  s.m = m; s.n = n; s.dlo = dls; s.D = Dband; s.alpha = alpha; s.beta = beta;
   s.mn = (A.variant & AGATHA_VAR_CHECK_LAST) ? m + n + 1 : m + n;  // Eq. 4 tested for c < mn
   s.zdrop = A.zdrop; s.B = -A.ref16; s.posValid = true;  // stored = X + alpha*c + ref16
   s.G_H = INT_MIN / 2; s.G_c = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.zthr = INT_MIN;
@@ -735,8 +749,13 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     s.zthr = A.zdrop >= 0 ? -A.zdrop : INT_MIN;
   }
   s.snapB = 0; s.snapPar = 0; s.snapTlo = 0; s.snapThi = 0; s.term = -1;
-  const int dlo = -bl, D = s.D;
+  const int dlo = -bl, D = Dband;
   const uint32_t AmB2 = pack2(alpha - beta, alpha - beta);
+  const int gend = off + D;  // first slot above the band (a multiple of NREG)
+  const bool wall_lo = (gend & (K - 1)) == NREG && lane == gend / K;
+  const bool wall_hi = lane == 31 || ((gend & (K - 1)) == 0 && lane == gend / K - 1);
+  const uint32_t KEEPX = (wall_lo ? 0u : 0xFFFFu) | (wall_hi ? 0u : 0xFFFF0000u);
+  const uint32_t LMK = (K * lane + K <= gend) ? 0xFFFFFFFFu : (K * lane + NREG <= gend ? 0xFFFFu : 0u);
 
   auto fdiag = [&](int d) { return 2 * min(m, n + d) - d; };
   const int dhi = br;
@@ -748,30 +767,30 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   // The first step computes anti-diagonal cb = 0 (even dlo) or 1 (odd dlo): the origin
   // and the first boundary cells come out of the DP itself, which starts the two gap
   // chains along the boundary (E of (i,0), F of (0,j)) that the masked steps carry.
-  int cb = dlo & 1;
-  int u = (cb + dlo) >> 1;
+  int cb = dls & 1;
+  int u = (cb + dls) >> 1;
   // boundary value of diagonal d (reading R2); slots beyond the band hold the cap
   auto bnd = [&](int d) { const int ad = d < 0 ? -d : d; return d == 0 ? 0 : -(alpha + (ad - 1) * beta); };
 
-  // a3: slot k of register j (j or j+NREG) on diagonal dlo + K*lane + k; a slot of
+  // a3: slot k of register j (j or j+NREG) on diagonal dls + K*lane + k; a slot of
   // parity(cb) holds anti-diagonal cb-2, the other parity cb-1 (both <= 0).  Slots start
   // at bnd(d) + alpha*c (stored units), diagonal 0 at the origin value 0, E/F at -inf;
   // DESIGN.md §6.2 "Masking" shows these reproduce the boundary exactly.
-  uint32_t H[NREG], E[NREG], F[NREG], CAP[NREG];
+  uint32_t H[NREG], E[NREG], F[NREG], CAP[NCAP];
   const uint32_t W2 = pack2(kW16, kW16);
 #pragma unroll
   for (int j = 0; j < NREG; ++j) {
     int v2[2], c2[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int k = j + h * NREG, g = K * lane + k, d = dlo + g;
-      const bool valid = g < D;
+      const int k = j + h * NREG, g = K * lane + k, d = dls + g;
+      const bool valid = g >= off && g < gend;
       c2[h] = valid ? 32767 : kCapNeg16;
-      const int ci = ((k & 1) == 0) ? cb - 2 : cb - 1;  // (dlo + K*lane) has parity of cb
+      const int ci = ((k & 1) == 0) ? cb - 2 : cb - 1;  // (dls + K*lane) has parity of cb
       v2[h] = valid ? (d == 0 ? 0 : bnd(d) + alpha * ci) - s.B : kCapNeg16;
     }
     H[j] = pack2(v2[0], v2[1]);
-    CAP[j] = pack2(c2[0], c2[1]);
+    if (j < NCAP) CAP[j < NCAP ? j : 0] = pack2(c2[0], c2[1]);
     E[j] = W2;
     F[j] = W2;
   }
@@ -780,7 +799,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   int wR = rpos >> 3, oR = rpos & 7;  // oR = 0
   uint32_t Wr0 = load_word_rw(Rw, wR, nwR), Wr1 = load_word_rw(Rw, wR + 1, nwR),
            Wr2 = load_word_rw(Rw, wR + 2, nwR);
-  int qpos = n + dlo - u + padQ + lane * NC;
+  int qpos = n + dls - u + padQ + lane * NC;
   int wQ = qpos >> 3, oQ = qpos & 7;  // oQ = 7 = 7 - oR from here on
   uint32_t Wq0 = load_word_rw(Qw, wQ, nwQ), Wq1 = load_word_rw(Qw, wQ + 1, nwQ),
            Wq2 = load_word_rw(Qw, wQ + 2, nwQ);
@@ -832,12 +851,12 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       scores(S2, Wr, qg, 4 * oR);
       int tlo = 0, thi = NC;
       if (MASKED) {
-        const int ib = u + lane * NC, jb = u - dlo - lane * NC;
+        const int ib = u + lane * NC, jb = u - dls - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 0, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one);
+      const int lmax = step16<NREG, NCAP, 0, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -850,12 +869,12 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       scores(S2, Wr, qg, 4 * oR + 4);
       int tlo = 0, thi = NC;
       if (MASKED) {
-        const int ib = u + 1 + lane * NC, jb = u - dlo - lane * NC;
+        const int ib = u + 1 + lane * NC, jb = u - dls - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, 1, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one);
+      const int lmax = step16<NREG, NCAP, 1, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
       const int rH = __reduce_max_sync(kFull, lmax);
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -931,8 +950,8 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int g = K * lane + k;
-    if (g < D) {
-      const int d = dlo + g;
+    if (g >= off && g < gend) {
+      const int d = dls + g;
       const int clo = (d < 0 ? -d : d) + 2;
       const int hi = min(fdiag(d), c_end);
       if (hi >= clo) cnt += ((hi - clo) >> 1) + 1;
@@ -950,7 +969,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   }
 }
 
-template <int NREG, bool TRACE>
+template <int NREG, bool TRACE, int NCAP>
 __global__ void __launch_bounds__(128, NREG >= 16 ? 3 : 4) align16_kernel(AlignArgs A) {
   __shared__ uint32_t snap_all[4][NREG / 2 * 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -959,7 +978,7 @@ __global__ void __launch_bounds__(128, NREG >= 16 ? 3 : 4) align16_kernel(AlignA
     if (lane == 0) q = atomicAdd(A.queue, 1);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
-    align_pair16<NREG, TRACE>(A, A.order[q], lane, snap_all[warp]);
+    align_pair16<NREG, TRACE, NCAP>(A, A.order[q], lane, snap_all[warp]);
   }
 }
 
@@ -987,6 +1006,7 @@ struct PrepArgs {
   uint8_t* bad;
   int* err_flags;   // bit 1: empty sequence, bit 2: out of range
   int* max_slots;   // max D over the batch
+  int* max_off16;   // max (-D) mod 16 over the batch (align16_kernel's low padding)
   const uint64_t* chunk_first;  // nchunks + 1 pair boundaries of the input chunks
   int nchunks;
   uint8_t* chunk_of;            // out: chunk of each pair
@@ -1035,7 +1055,10 @@ __global__ void prep_kernel(PrepArgs P) {
       }
       P.bad[p] = (uint8_t)(flag != 0);
       if (flag) atomicOr(P.err_flags, flag);
-      else atomicMax(P.max_slots, (int)D);
+      else {
+        atomicMax(P.max_slots, (int)D);
+        atomicMax(P.max_off16, (int)((-D) & 15));
+      }
     }
   }
 }
@@ -1161,11 +1184,11 @@ void score_table16(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
   *T1 = t[4] | (t[5] << 8) | (t[6] << 16) | ((uint32_t)t[7] << 24);
 }
 
-template <int NREG, bool TRACE>
+template <int NREG, bool TRACE, int NCAP>
 int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
   static int occ = -1;
   if (occ < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align16_kernel<NREG, TRACE>, 128, 0) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align16_kernel<NREG, TRACE, NCAP>, 128, 0) != cudaSuccess) {
       cudaGetLastError();
       occ = 1;
     }
@@ -1176,7 +1199,7 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
   int grid = (int)(want < need ? want : need);
   if (grid < 1) grid = 1;
   *grid_out = grid;
-  align16_kernel<NREG, TRACE><<<grid, 128, 0, st>>>(A);
+  align16_kernel<NREG, TRACE, NCAP><<<grid, 128, 0, st>>>(A);
   CUDA_TRY(cudaGetLastError());
   return AGATHA_OK;
 }
@@ -1282,7 +1305,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     if ((rc = grow(ctx->results, sizeof(agatha_result_t) * P))) return rc;
     d_out = (agatha_result_t*)ctx->results.p;
   }
-  int* d_sc = (int*)ctx->scalars.p;  // [0] err_flags [1] max_slots [2] queue
+  int* d_sc = (int*)ctx->scalars.p;  // [0] err_flags [1] max_slots [2] queue [3] max (-D) mod 16
   int* d_ready = (int*)ctx->ready.p;
   CUDA_TRY(cudaMemsetAsync(d_sc, 0, 16, st));
   CUDA_TRY(cudaMemcpyAsync(ctx->chunk_first.p, ctx->h_chunk_first, 8 * (nchunks + 1),
@@ -1297,7 +1320,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   pa.bl = p->band_left; pa.br = p->band_right; pa.alpha = p->gap_open; pa.beta = p->gap_extend;
   pa.maxs = maxs;
   pa.nominal = (uint32_t*)ctx->nominal.p; pa.iota = (uint32_t*)ctx->iota.p;
-  pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1;
+  pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1; pa.max_off16 = d_sc + 3;
   pa.chunk_first = (const uint64_t*)ctx->chunk_first.p; pa.nchunks = nchunks;
   pa.chunk_of = (uint8_t*)ctx->chunk_of.p; pa.key64 = (uint64_t*)ctx->key64.p;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
@@ -1317,9 +1340,9 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     lib_launches = 4;
   }
   // K (slots per lane) from the widest band in the batch
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 16, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  const int err0 = ctx->h_scalars[0], maxD = ctx->h_scalars[1];
+  const int err0 = ctx->h_scalars[0], maxD = ctx->h_scalars[1], maxoff16 = ctx->h_scalars[3];
   if (err0 & 2) return AGATHA_EEMPTY;
   if (err0 & 4) return AGATHA_ERANGE;
   CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
@@ -1344,8 +1367,12 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   const bool k16 = use16(p, maxD) && !(b->flags & AGATHA_FORCE_32BIT);
   const bool tr = trace_pair >= 0;
   if (k16) {
-    if (K == 16) rc = tr ? launch_align16<8, true>(ctx, A, st, &grid) : launch_align16<8, false>(ctx, A, st, &grid);
-    else rc = tr ? launch_align16<16, true>(ctx, A, st, &grid) : launch_align16<16, false>(ctx, A, st, &grid);
+    // (NREG = 16) eight capped registers suffice when every pair's low padding
+    // off = (-D) mod 16 is at most 8 (prep_kernel's max); else all sixteen
+    if (K == 16) rc = tr ? launch_align16<8, true, 8>(ctx, A, st, &grid) : launch_align16<8, false, 8>(ctx, A, st, &grid);
+    else if (tr) rc = launch_align16<16, true, 16>(ctx, A, st, &grid);
+    else if (maxoff16 <= 8) rc = launch_align16<16, false, 8>(ctx, A, st, &grid);
+    else rc = launch_align16<16, false, 16>(ctx, A, st, &grid);
   } else {
     if (K == 16) rc = tr ? launch_align<16, true>(ctx, A, st, &grid) : launch_align<16, false>(ctx, A, st, &grid);
     else rc = tr ? launch_align<32, true>(ctx, A, st, &grid) : launch_align<32, false>(ctx, A, st, &grid);
@@ -1528,7 +1555,7 @@ int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* b, const agatha_params_
   pa.bl = p->band_left; pa.br = p->band_right; pa.alpha = p->gap_open; pa.beta = p->gap_extend;
   pa.maxs = maxs;
   pa.nominal = nominal; pa.iota = (uint32_t*)ctx->iota.p;
-  pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1;
+  pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1; pa.max_off16 = d_sc + 3;
   pa.chunk_first = nullptr; pa.nchunks = 1; pa.chunk_of = nullptr; pa.key64 = nullptr;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);

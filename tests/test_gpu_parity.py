@@ -57,6 +57,36 @@ def test_random_short_pairs(gpu_lib, ctx, kflags, band):
         compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=band, band_right=band, zdrop=z), flags=kflags)
 
 
+# Band sizes D = bl + br + 1 that put the 16-bit kernel's low padding off = (-D) mod NREG
+# at every interesting value, for both NREG = 8 (D <= 512) and NREG = 16 (D <= 1024, the
+# eight-cap kernel for off <= 8 and the sixteen-cap one above): DESIGN.md §6.1 "Layout".
+@pytest.mark.parametrize("bl,br", [(256, 255), (255, 255), (250, 255), (249, 254), (100, 3),
+                                   (504, 504), (503, 504), (500, 500), (300, 292), (511, 511),
+                                   (511, 500), (0, 600), (600, 0), (264, 264)])
+def test_band_layouts_long_pairs(gpu_lib, ctx, bl, br):
+    rng = np.random.default_rng(7000 + bl * 1000 + br)
+    lst = []
+    for k in range(48):
+        m = int(rng.integers(700, 1400))
+        a = "".join("ACGT"[x] for x in rng.integers(0, 4, m))
+        q = list(a)
+        for t in range(len(q)):
+            if rng.random() < 0.03:
+                q[t] = "ACGT"[int(rng.integers(0, 4))]
+        q = "".join(q)
+        if k % 3 == 1:  # an indel that moves the path towards a band edge
+            x = int(rng.integers(100, 400))
+            q = q[:x] + q[x + int(rng.integers(5, 60)):]
+        if k % 3 == 2:
+            x = int(rng.integers(100, 400))
+            q = q[:x] + "".join("ACGT"[y] for y in rng.integers(0, 4, int(rng.integers(5, 60)))) + q[x:]
+        lst.append((a, q))
+    pairs = synth.from_list(lst)
+    for z in (-1, 100):
+        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=bl, band_right=br, zdrop=z))
+        assert ctx.stats()["packed16"] == 1
+
+
 def test_asymmetric_bands_and_penalties(gpu_lib, ctx, kflags):
     rng = np.random.default_rng(77)
     pairs = synth.random_short_pairs(rng, 200, 300)
