@@ -1362,6 +1362,25 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   score_table(p, &A.T0, &A.T1);
   score_table16(p, &A.T16_0, &A.T16_1);
   A.trace_pair = trace_pair; A.trace_score = trace_score; A.trace_i = trace_i; A.trace_cap = trace_cap;
+  if (!dev_in) {
+    // stream the ASCII in chunk by chunk while the kernel runs; each chunk's flag is
+    // written after its bytes (same stream), and the kernel reads it with acquire.
+    // The copies are enqueued before the kernel so that a launch that blocks the host
+    // (CUDA_LAUNCH_BLOCKING, a serialising profiler) cannot wait on flags not yet issued.
+    CUDA_TRY(cudaEventRecord(ctx->cev[0], ctx->copy_stream));
+    for (int c = 0; c < nchunks; ++c) {
+      const uint64_t k0 = ctx->h_chunk_first[c], k1 = ctx->h_chunk_first[c + 1];
+      const uint64_t rb = b->ref_off[k0], re = b->ref_off[k1], qb = b->qry_off[k0], qe = b->qry_off[k1];
+      if (re > rb)
+        CUDA_TRY(cudaMemcpyAsync((uint8_t*)ctx->ref_ascii.p + rb, b->ref + rb, re - rb,
+                                 cudaMemcpyHostToDevice, ctx->copy_stream));
+      if (qe > qb)
+        CUDA_TRY(cudaMemcpyAsync((uint8_t*)ctx->qry_ascii.p + qb, b->qry + qb, qe - qb,
+                                 cudaMemcpyHostToDevice, ctx->copy_stream));
+      CUDA_TRY(cudaMemcpyAsync(d_ready + c, ctx->h_ones, 4, cudaMemcpyHostToDevice, ctx->copy_stream));
+    }
+    CUDA_TRY(cudaEventRecord(ctx->cev[1], ctx->copy_stream));
+  }
   int grid = 0;
   const int K = maxD <= 512 ? 16 : 32;
   const bool k16 = use16(p, maxD) && !(b->flags & AGATHA_FORCE_32BIT);
@@ -1378,25 +1397,11 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     else rc = tr ? launch_align<32, true>(ctx, A, st, &grid) : launch_align<32, false>(ctx, A, st, &grid);
   }
   ctx->stats.packed16 = k16 ? 1 : 0;
-  if (rc) return rc;
-  ++launches;
-  if (!dev_in) {
-    // stream the ASCII in chunk by chunk while the kernel runs; each chunk's flag is
-    // written after its bytes (same stream), and the kernel reads it with acquire
-    CUDA_TRY(cudaEventRecord(ctx->cev[0], ctx->copy_stream));
-    for (int c = 0; c < nchunks; ++c) {
-      const uint64_t k0 = ctx->h_chunk_first[c], k1 = ctx->h_chunk_first[c + 1];
-      const uint64_t rb = b->ref_off[k0], re = b->ref_off[k1], qb = b->qry_off[k0], qe = b->qry_off[k1];
-      if (re > rb)
-        CUDA_TRY(cudaMemcpyAsync((uint8_t*)ctx->ref_ascii.p + rb, b->ref + rb, re - rb,
-                                 cudaMemcpyHostToDevice, ctx->copy_stream));
-      if (qe > qb)
-        CUDA_TRY(cudaMemcpyAsync((uint8_t*)ctx->qry_ascii.p + qb, b->qry + qb, qe - qb,
-                                 cudaMemcpyHostToDevice, ctx->copy_stream));
-      CUDA_TRY(cudaMemcpyAsync(d_ready + c, ctx->h_ones, 4, cudaMemcpyHostToDevice, ctx->copy_stream));
-    }
-    CUDA_TRY(cudaEventRecord(ctx->cev[1], ctx->copy_stream));
+  if (rc) {
+    if (!dev_in) cudaStreamSynchronize(ctx->copy_stream);
+    return rc;
   }
+  ++launches;
   CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
   if (!dev_out)
     CUDA_TRY(cudaMemcpyAsync(out, d_out, sizeof(agatha_result_t) * P, cudaMemcpyDeviceToHost, st));
