@@ -48,7 +48,7 @@ SM_COUNT = 148
 LANES_PER_CLK_PER_SM = 64
 # dram__bytes_read.sum + dram__bytes_write.sum per align launch on the full C2 batch, from
 # one `ncu --set full` capture (profiles/r01_ncu_*_summary.csv); updated per profile.
-TRAFFIC = {"align_kernel<32>": 1.603e9 + 0.0748e9, "align16_kernel<16>": 3.346e9 + 1.505e9}
+TRAFFIC = {"align_kernel<32>": 1.603e9 + 0.0748e9, "align16_kernel<16>": 3.324e9 + 1.506e9}
 
 
 def parse():
@@ -284,7 +284,8 @@ def main():
     f_ghz = (clocks["sm_max_mhz"] or 1965) / 1e3
     peak_tops = SM_COUNT * LANES_PER_CLK_PER_SM * f_ghz * 1e9 / 1e12
     achieved_tops = OPS_PER_CELL * cells_rank / (align_avg_ms / 1e3) / 1e12
-    kname = "align16_kernel<16>" if stats.get("packed16") else f"align_kernel<{stats['slots_per_lane']}>"
+    kname = (f"align16_kernel<{stats['slots_per_lane'] // 2}>" if stats.get("packed16")
+             else f"align_kernel<{stats['slots_per_lane']}>")
     roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops,
                 "unit": "T ALU lane-instr/s", "frac": achieved_tops / peak_tops,
                 "traffic": TRAFFIC.get(kname), "traffic_unit": "bytes/launch (ncu dram read+write)",
