@@ -18,7 +18,9 @@ edge = synth.from_list([("A", "A"), ("ACGT" * 300, "A"), ("A", "ACGT" * 300), ("
 for p in (pairs, edge):
     for flags in (0, agatha.FORCE_32BIT, agatha.ORDER_INPUT):
         for prm in (vars(cfg.scoring), dict(vars(cfg.scoring), band_left=500, band_right=500, zdrop=-1),
-                    dict(vars(cfg.scoring), band_left=0, band_right=3)):
+                    dict(vars(cfg.scoring), band_left=504, band_right=504, zdrop=300),
+                    dict(vars(cfg.scoring), band_left=0, band_right=3),
+                    dict(vars(cfg.scoring), band_left=0, band_right=0)):
             agatha.align_pairs(ctx, p, prm, flags=flags)
 R, Q = pairs.pair(3)
 agatha.localmax_trace(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, vars(cfg.scoring), 3,
