@@ -44,6 +44,8 @@ import synth  # noqa: E402
 # B300_MICROARCH "alu-pipe rt_SMSP=2"; measured 62.4-62.5, profiles/r01_dpx16.jsonl) x
 # clocks.max.sm.
 OPS_PER_CELL = 2.25
+# the same minimal formulation one cell per lane-instruction (the 32-bit kernels)
+OPS_PER_CELL_32 = 4.5
 SM_COUNT = 148
 LANES_PER_CLK_PER_SM = 64
 # dram__bytes_read.sum + dram__bytes_write.sum per align launch on the full C2 batch, from
@@ -283,16 +285,21 @@ def main():
     clocks = clk.summary()
     f_ghz = (clocks["sm_max_mhz"] or 1965) / 1e3
     peak_tops = SM_COUNT * LANES_PER_CLK_PER_SM * f_ghz * 1e9 / 1e12
-    achieved_tops = OPS_PER_CELL * cells_rank / (align_avg_ms / 1e3) / 1e12
-    kname = (f"align16_kernel<{stats['slots_per_lane'] // 2}>" if stats.get("packed16")
-             else f"align_kernel<{stats['slots_per_lane']}>")
+    ops = OPS_PER_CELL if stats.get("packed16") else OPS_PER_CELL_32
+    achieved_tops = ops * cells_rank / (align_avg_ms / 1e3) / 1e12
+    if stats.get("packed16"):
+        kname = f"align16_kernel<{stats['slots_per_lane'] // 2}>"
+    elif stats.get("warps_per_pair", 1) > 1:
+        kname = f"align_wide_kernel<{stats['warps_per_pair']}>"
+    else:
+        kname = f"align_kernel<{stats['slots_per_lane']}>"
     roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops,
                 "unit": "T ALU lane-instr/s", "frac": achieved_tops / peak_tops,
                 "traffic": TRAFFIC.get(kname), "traffic_unit": "bytes/launch (ncu dram read+write)",
                 "kernel": kname, "kernel_ms": align_avg_ms,
                 "kernel_gcups": cells_rank / (align_avg_ms / 1e3) / 1e9,
-                "gcups_roof": peak_tops * 1e12 / OPS_PER_CELL / 1e9,
-                "ops_per_cell": OPS_PER_CELL,
+                "gcups_roof": peak_tops * 1e12 / ops / 1e9,
+                "ops_per_cell": ops,
                 "peak_basis": f"148 SM x 64 ALU lanes/clk x {f_ghz:.3f} GHz (clocks.max.sm); "
                               "ops_per_cell = minimal DPX .S16x2 ALU lane-instructions per cell"}
 

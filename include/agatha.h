@@ -36,7 +36,7 @@ extern "C" {
 #define AGATHA_EINVAL (-1) /* invalid scoring parameters or arguments  */
 #define AGATHA_EEMPTY (-2) /* a sequence of length 0 or n_pairs == 0 */
 #define AGATHA_ECHAR (-3)  /* a non-ACGTN byte under AGATHA_N_REJECT         */
-#define AGATHA_ERANGE (-4) /* band wider than 1024 diagonals, penalties > 127, or a pair so
+#define AGATHA_ERANGE (-4) /* band wider than 4096 diagonals, penalties > 127, or a pair so
                               long that |H| could reach 2^20         */
 #define AGATHA_ECUDA (-5)  /* CUDA runtime failure / no sm_100a device                    */
 #define AGATHA_ENOMEM (-6) /* device allocation failed                                    */
@@ -107,6 +107,7 @@ typedef struct {
   int32_t kernel_launches; /* kernels of this library launched by the call              */
   int32_t library_launches; /* CUB radix-sort kernels launched by the call             */
   int32_t packed16;    /* 1 if the 16-bit packed (DPX .S16x2) kernel ran, 0 for 32-bit    */
+  int32_t warps_per_pair; /* 1; 2 or 4 in the wide-band tier (D > 1024, 32-bit)          */
 } agatha_stats_t;
 
 /* Create a context on CUDA device `cuda_device`.  Fails with AGATHA_ECUDA when the

@@ -55,7 +55,7 @@ class Stats(ctypes.Structure):
                 ("align_ms", ctypes.c_float), ("d2h_ms", ctypes.c_float),
                 ("slots_per_lane", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
                 ("kernel_launches", ctypes.c_int32), ("library_launches", ctypes.c_int32),
-                ("packed16", ctypes.c_int32)]
+                ("packed16", ctypes.c_int32), ("warps_per_pair", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -42,7 +42,9 @@ constexpr int kPadH = -(1 << 21);       // initial H of a padding slot
 constexpr int kNegKey = -(1 << 30);     // key of a cell outside the table
 constexpr int kEmptyH = -kHLimit;       // lane max H at or below this: no cell on the diagonal
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kMaxSlots = 1024;         // 32 lanes x 32 slots
+constexpr int kMaxSlots = 1024;         // one warp: 32 lanes x 32 slots (the 16-bit kernel)
+constexpr int kMaxWarpsWide = 4;        // wide-band tier: up to 4 warps per pair (NEXT #3)
+constexpr int kMaxSlotsWide = kMaxWarpsWide * kMaxSlots;
 constexpr int kMaxChunks = 255;         // input chunks of one call (chunk ids are uint8)
 constexpr uint64_t kChunkBytes = 48ull << 20;  // target ASCII bytes per streamed chunk
 
@@ -157,19 +159,20 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void pack_pair_fused(const uint8_t* __restrict__ ref, const uint8_t* __restrict__ qry,
                                                 uint64_t r0, uint64_t q0, int m, int n, uint32_t* Rw,
                                                 uint32_t* Qw, const int* ready, int chunk, bool nmap,
-                                                int* err_flags, int lane, int padR = 0, int padQ = 0) {
+                                                int* err_flags, int lane, int padR = 0, int padQ = 0,
+                                                int stride = 32) {
   if (ready) {
     while (ld_acquire(ready + chunk) == 0) __nanosleep(500);
   }
   int err = 0;
   const int nwR = (m + padR + 7) / 8, nwQ = (n + padQ + 7) / 8;
-  for (int w = lane; w < nwR; w += 32) Rw[1 + w] = pack_word(ref + r0, m, w, false, nmap, &err, padR, 8u);
-  for (int w = lane; w < nwQ; w += 32) Qw[1 + w] = pack_word(qry + q0, n, w, true, nmap, &err, padQ, 8u);
+  for (int w = lane; w < nwR; w += stride) Rw[1 + w] = pack_word(ref + r0, m, w, false, nmap, &err, padR, 8u);
+  for (int w = lane; w < nwQ; w += stride) Qw[1 + w] = pack_word(qry + q0, n, w, true, nmap, &err, padQ, 8u);
   if (lane == 0) {
     Rw[0] = kOutWord; Rw[nwR + 1] = kOutWord;
     Qw[0] = kOutWord; Qw[nwQ + 1] = kOutWord;
   }
-  if (__any_sync(kFull, err) && lane == 0) atomicOr(err_flags, 1);
+  if (__any_sync(kFull, err) && (lane & 31) == 0) atomicOr(err_flags, 1);
   __syncwarp();
 }
 
@@ -244,20 +247,23 @@ __device__ __forceinline__ bool process_antidiag(PairState& s, const AlignArgs& 
 //   Eh(i,j) = max(Eh(i-1,j) - beta, H(i-1,j))      [= Eq. 2 + alpha]
 //   Fh(i,j) = max(Fh(i,j-1) - beta, H(i,j-1))      [= Eq. 3 + alpha]
 //   H(i,j)  = max(max(Eh, Fh) - alpha, H(i-1,j-1) + S)   [= Eq. 1]
+// edgeH / edgeEF: the neighbour of the warp's edge lane (lane 0 for PAR = 0, lane 31 for
+// PAR = 1): -infinity at the band's ends, the adjacent warp's slot in the wide tier.
 template <int K, int PAR, bool MASKED>
 __device__ __forceinline__ int step_cells(int (&H)[K], int (&Eh)[K], int (&Fh)[K],
                                           const uint32_t (&S)[K / 8], int lane, int nalpha,
-                                          int nbeta, int capT, int tlo, int thi, int sixteen) {
+                                          int nbeta, int capT, int tlo, int thi, int sixteen,
+                                          int edgeH = kNegE, int edgeEF = kNegE) {
   // edge exchange: the one neighbour slot that lives in the adjacent lane
   int xH, xEF;
   if (PAR == 0) {
     xH = __shfl_up_sync(kFull, H[K - 1], 1);
     xEF = __shfl_up_sync(kFull, Eh[K - 1], 1);
-    if (lane == 0) { xH = kNegE; xEF = kNegE; }   // below the band: -infinity
+    if (lane == 0) { xH = edgeH; xEF = edgeEF; }    // below the band (or the previous warp)
   } else {
     xH = __shfl_down_sync(kFull, H[0], 1);
     xEF = __shfl_down_sync(kFull, Fh[0], 1);
-    if (lane == 31) { xH = kNegE; xEF = kNegE; }  // above the last lane: -infinity
+    if (lane == 31) { xH = edgeH; xEF = edgeEF; }   // above the band (or the next warp)
   }
   int lk = kNegKey, kprev = kNegKey;
 #pragma unroll
@@ -469,6 +475,268 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignAr
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
     align_pair<K, TRACE>(A, A.order[q], lane);
+  }
+}
+
+
+// ---- NEXT #3: the wide-band tier (32-bit, W warps per pair) --------------------------
+// Bands wider than one warp's 1024 slots (w > 511) split the D <= 1024*W diagonals over
+// the 32*W lanes of a W-warp block in order (global lane gl = 32*warp + lane; K = 32
+// slots each).  Per step, the two warp-edge slots cross warps through shared memory and
+// each warp publishes its anti-diagonal max with the diagonal of its first maximal cell;
+// one __syncthreads orders both (two per iteration).  Every Eq. 4-6 decision is taken
+// from the block-wide values, identically in all warps, so control flow stays
+// block-uniform.  Same cells, same arithmetic, same results as align_kernel.
+struct WideShared {
+  int up_H[kMaxWarpsWide], up_E[kMaxWarpsWide];   // lane 31's slot K-1 after a PAR = 1 step
+  int dn_H[kMaxWarpsWide], dn_F[kMaxWarpsWide];   // lane 0's slot 0 after a PAR = 0 step
+  int rH[2][kMaxWarpsWide], d[2][kMaxWarpsWide];  // per step parity: warp max, its diagonal
+  int cnt[kMaxWarpsWide];
+  int q;
+};
+
+// Eq. 4 / Eq. 6 for anti-diagonal c given the block-wide max rH and the diagonal d of its
+// first (smallest i) maximal cell; true when Eq. 4 fires.
+template <bool TRACE>
+__device__ __forceinline__ bool process_wide(PairState& s, const AlignArgs& A, int c, int rH, int d,
+                                             bool leader, long long pid) {
+  if (rH <= kEmptyH) return false;  // empty anti-diagonal: skipped (reading R11)
+  const bool upd = !s.haveG || rH > s.G_H;
+  const int c_end = (A.variant & AGATHA_VAR_CHECK_LAST) ? s.m + s.n + 1 : s.m + s.n;
+  const bool chk = s.haveG && A.zdrop >= 0 && (s.G_H - rH > A.zdrop) && (c < c_end);
+  if (!(upd || chk || TRACE)) return false;
+  const int i = (c + d) >> 1;
+  const int j = c - i;
+  if (TRACE && leader && pid == A.trace_pair && c < A.trace_cap) {
+    A.trace_score[c] = rH;
+    A.trace_i[c] = i;
+  }
+  const bool gated = (A.variant & AGATHA_VAR_GATE_GE) ? (s.G_i <= i && s.G_j <= j)
+                                                       : (s.G_i < i && s.G_j < j);
+  if (chk && gated) {
+    const int gap = d - s.G_d;
+    if (s.G_H - rH > A.zdrop + A.beta * (gap < 0 ? -gap : gap)) {
+      s.term = c;
+      return true;
+    }
+  }
+  if (upd) {
+    s.G_H = rH;
+    s.G_i = i;
+    s.G_j = j;
+    s.G_d = d;
+    s.haveG = true;
+  }
+  return false;
+}
+
+template <int W, bool TRACE>
+__device__ void align_pair_wide(const AlignArgs& A, uint32_t pid, int lane, int wid, WideShared& sh) {
+  constexpr int K = 32;
+  const int gl = wid * 32 + lane;
+  const uint64_t r0 = A.roff[pid], q0 = A.qoff[pid];
+  const int m = (int)(A.roff[pid + 1] - r0);
+  const int n = (int)(A.qoff[pid + 1] - q0);
+  if (A.bad[pid]) {  // block-uniform
+    if (gl == 0) {
+      agatha_result_t z = {0, 0, 0, -1, 0};
+      A.out[pid] = z;
+    }
+    return;
+  }
+  uint32_t* Rw = A.rw + (r0 >> 3) + 4 * pid;
+  uint32_t* Qw = A.qw + (q0 >> 3) + 4 * pid;
+  const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
+  pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
+                  A.nmap != 0, A.err_flags, gl, 0, 0, 32 * W);
+  const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;
+  const int br = (A.br < 0 || A.br > m) ? m : A.br;
+  const int alpha = A.alpha, beta = A.beta, nbeta = -A.beta, nalpha = -A.alpha;
+
+  PairState s;
+  s.m = m; s.n = n; s.dlo = -bl; s.D = bl + br + 1;
+  s.haveG = (A.variant & AGATHA_VAR_ORIGIN_MAX) != 0;  // G = H(0,0) = 0 at the origin
+  s.G_H = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.term = -1;
+  const int dlo = -bl, D = s.D;
+
+  // padding cap: slot k of this lane is capped at capT - k*kCapStep
+  const int gbase = gl * K;
+  int capT;
+  if (gbase + K <= D) capT = 1 << 30;
+  else if (gbase >= D) capT = -kHLimit;
+  else capT = (D - gbase - 1) * kCapStep + kHLimit;
+
+  int H[K], Eh[K], Fh[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int g = gbase + k, d = dlo + g;
+    const int ad = d < 0 ? -d : d;
+    H[k] = (g < D) ? (d == 0 ? 0 : -(alpha + (ad - 1) * beta)) : kPadH;
+    Eh[k] = kNegE;
+    Fh[k] = kNegE;
+  }
+  if (lane == 31) { sh.up_H[wid] = H[K - 1]; sh.up_E[wid] = Eh[K - 1]; }
+  __syncthreads();  // the packed words and the first edge values are visible block-wide
+
+  auto fdiag = [&](int d) { return 2 * min(m, n + d) - d; };
+  const int dhi = br;
+  const int cs = 2 + max(bl, br);
+  const int ce = min(fdiag(dlo), fdiag(dhi));
+  const int dmid = min(max(m - n, dlo), dhi);
+  const int c_last = fdiag(dmid);
+
+  int cb = 2 - (dlo & 1);
+  int u = (cb + dlo) >> 1;
+  int rpos = u - 1 + gl * (K / 2);
+  int wR = rpos >> 3, oR = rpos & 7;
+  uint32_t Wr0 = load_word_rw(Rw, wR, nwR), Wr1 = load_word_rw(Rw, wR + 1, nwR),
+           Wr2 = load_word_rw(Rw, wR + 2, nwR);
+  int qpos = n + dlo - u + gl * (K / 2);
+  int wQ = qpos >> 3, oQ = qpos & 7;
+  uint32_t Wq0 = load_word_rw(Qw, wQ, nwQ), Wq1 = load_word_rw(Qw, wQ + 1, nwQ),
+           Wq2 = load_word_rw(Qw, wQ + 2, nwQ);
+  const uint32_t T0 = A.T0, T1 = A.T1;
+  bool stop = false;
+
+  // warp max and the diagonal of its first maximal cell (smallest lane, then slot)
+  auto publish = [&](int lk, int par) {
+    const int wmax = __reduce_max_sync(kFull, lk >> 4);
+    const unsigned bal = __ballot_sync(kFull, (lk >> 4) == wmax);
+    const int ls = __ffs(bal) - 1;
+    const int kk = __shfl_sync(kFull, lk, ls);
+    const int t = 15 - (kk & 15);
+    if (lane == 0) {
+      sh.rH[par][wid] = wmax;
+      sh.d[par][wid] = dlo + (wid * 32 + ls) * K + par + 2 * t;
+    }
+  };
+  // block max (warps in diagonal order: the first warp holding it has the smallest d)
+  auto combine_warps = [&](int par, int& rH, int& d) {
+    rH = sh.rH[par][0];
+    d = sh.d[par][0];
+#pragma unroll
+    for (int w = 1; w < W; ++w) {
+      const int v = sh.rH[par][w];
+      if (v > rH) { rH = v; d = sh.d[par][w]; }
+    }
+  };
+
+  auto iteration = [&](auto masked_tag) {
+    constexpr bool MASKED = decltype(masked_tag)::value;
+    uint32_t qg[2], S[4];
+    const uint32_t Wq[3] = {Wq0, Wq1, Wq2}, Wr[3] = {Wr0, Wr1, Wr2};
+#pragma unroll
+    for (int g = 0; g < 2; ++g) qg[g] = __funnelshift_rc(Wq[g], Wq[g + 1], 4 * oQ);
+    // ---- step PAR = 0, anti-diagonal cb ----
+    {
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const uint32_t x = combine(__funnelshift_rc(Wr[g], Wr[g + 1], 4 * oR), qg[g]);
+        S[2 * g] = prmt(T0, T1, x);
+        S[2 * g + 1] = prmt(T0, T1, x >> 16);
+      }
+      int tlo = 0, thi = K;
+      if (MASKED) {
+        const int ib = u + gl * (K / 2), jb = u - dlo - gl * (K / 2);
+        tlo = max(1 - ib, jb - n);
+        thi = min(m - ib, jb - 1);
+      }
+      const int eH = wid > 0 ? sh.up_H[wid > 0 ? wid - 1 : 0] : kNegE;
+      const int eE = wid > 0 ? sh.up_E[wid > 0 ? wid - 1 : 0] : kNegE;
+      const int lk = step_cells<K, 0, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi,
+                                              A.sixteen, eH, eE);
+      publish(lk, 0);
+      if (lane == 0) { sh.dn_H[wid] = H[0]; sh.dn_F[wid] = Fh[0]; }
+      __syncthreads();
+      int rH, d;
+      combine_warps(0, rH, d);
+      if (process_wide<TRACE>(s, A, cb, rH, d, gl == 0, pid)) { stop = true; return; }
+    }
+    // ---- step PAR = 1, anti-diagonal cb + 1 ----
+    {
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const uint32_t x = combine(__funnelshift_rc(Wr[g], Wr[g + 1], 4 * oR + 4), qg[g]);
+        S[2 * g] = prmt(T0, T1, x);
+        S[2 * g + 1] = prmt(T0, T1, x >> 16);
+      }
+      int tlo = 0, thi = K;
+      if (MASKED) {
+        const int ib = u + 1 + gl * (K / 2), jb = u - dlo - gl * (K / 2);
+        tlo = max(1 - ib, jb - n);
+        thi = min(m - ib, jb - 1);
+      }
+      const int eH = wid < W - 1 ? sh.dn_H[wid < W - 1 ? wid + 1 : 0] : kNegE;
+      const int eF = wid < W - 1 ? sh.dn_F[wid < W - 1 ? wid + 1 : 0] : kNegE;
+      const int lk = step_cells<K, 1, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi,
+                                              A.sixteen, eH, eF);
+      publish(lk, 1);
+      if (lane == 31) { sh.up_H[wid] = H[K - 1]; sh.up_E[wid] = Eh[K - 1]; }
+      __syncthreads();
+      int rH, d;
+      combine_warps(1, rH, d);
+      if (process_wide<TRACE>(s, A, cb + 1, rH, d, gl == 0, pid)) { stop = true; return; }
+    }
+    cb += 2;
+    ++u;
+    if (++oR == 8) {
+      oR = 0;
+      ++wR;
+      Wr0 = Wr1; Wr1 = Wr2; Wr2 = load_word_rw(Rw, wR + 2, nwR);
+    }
+    if (--oQ < 0) {
+      oQ = 7;
+      --wQ;
+      Wq2 = Wq1; Wq1 = Wq0; Wq0 = load_word_rw(Qw, wQ, nwQ);
+    }
+  };
+
+  while (!stop && cb <= c_last && cb < cs) iteration(TrueT{});
+  while (!stop && cb + 1 <= ce) iteration(FalseT{});
+  while (!stop && cb <= c_last) iteration(TrueT{});
+
+  // a8: cells on anti-diagonals 2 .. c_end (closed form per slot), summed over the block
+  const int c_end = s.term >= 0 ? s.term : m + n;
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int g = gbase + k;
+    if (g < D) {
+      const int d = dlo + g;
+      const int clo = (d < 0 ? -d : d) + 2;
+      const int hi = min(fdiag(d), c_end);
+      if (hi >= clo) cnt += ((hi - clo) >> 1) + 1;
+    }
+  }
+  cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
+  if (lane == 0) sh.cnt[wid] = cnt;
+  __syncthreads();
+  if (gl == 0) {
+    long long tot = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) tot += sh.cnt[w];
+    agatha_result_t r;
+    r.score = s.G_H;
+    r.ref_end = s.G_i;
+    r.query_end = s.G_j;
+    r.zdrop_antidiag = s.term;
+    r.cells = tot;
+    A.out[pid] = r;
+  }
+}
+
+// 12 warps per SM as for align_kernel<32> (~168 registers).
+template <int W, bool TRACE>
+__global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A) {
+  __shared__ WideShared sh;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) sh.q = atomicAdd(A.queue, 1);
+    __syncthreads();
+    const int q = sh.q;
+    __syncthreads();  // every thread has read q before thread 0 takes the next one
+    if ((uint32_t)q >= A.n_pairs) break;
+    align_pair_wide<W, TRACE>(A, A.order[q], lane, wid, sh);
   }
 }
 
@@ -1028,7 +1296,7 @@ __global__ void prep_kernel(PrepArgs P) {
     // |H| bound: alpha + max(bl,br)*beta + max(a,b,n)*min(m,n)
     const int64_t hb = (int64_t)P.alpha + (bl > br ? bl : br) * (int64_t)P.beta +
                        (int64_t)P.maxs * (m < n ? m : n);
-    if (!flag && (D > kMaxSlots || hb >= kHLimit - 16 || m + n >= (1LL << 30))) flag = 4;
+    if (!flag && (D > kMaxSlotsWide || hb >= kHLimit - 16 || m + n >= (1LL << 30))) flag = 4;
     // nominal in-band in-table cells: sum over diagonals d of |{i : 1<=i<=m, 1<=i-d<=n}|
     uint64_t cnt = 0;
     if (!flag) {
@@ -1200,6 +1468,26 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
   if (grid < 1) grid = 1;
   *grid_out = grid;
   align16_kernel<NREG, TRACE, NCAP><<<grid, 128, 0, st>>>(A);
+  CUDA_TRY(cudaGetLastError());
+  return AGATHA_OK;
+}
+
+template <int W, bool TRACE>
+int launch_align_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
+  static int occ = -1;
+  if (occ < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align_wide_kernel<W, TRACE>, 32 * W, 0) != cudaSuccess) {
+      cudaGetLastError();
+      occ = 1;
+    }
+    if (occ < 1) occ = 1;
+  }
+  const long long want = (long long)ctx->num_sms * occ;  // persistent: one pair per block
+  const long long need = (long long)A.n_pairs;
+  int grid = (int)(want < need ? want : need);
+  if (grid < 1) grid = 1;
+  *grid_out = grid;
+  align_wide_kernel<W, TRACE><<<grid, 32 * W, 0, st>>>(A);
   CUDA_TRY(cudaGetLastError());
   return AGATHA_OK;
 }
@@ -1394,7 +1682,10 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     else rc = launch_align16<16, false, 16>(ctx, A, st, &grid);
   } else {
     if (K == 16) rc = tr ? launch_align<16, true>(ctx, A, st, &grid) : launch_align<16, false>(ctx, A, st, &grid);
-    else rc = tr ? launch_align<32, true>(ctx, A, st, &grid) : launch_align<32, false>(ctx, A, st, &grid);
+    else if (maxD <= kMaxSlots) rc = tr ? launch_align<32, true>(ctx, A, st, &grid) : launch_align<32, false>(ctx, A, st, &grid);
+    else if (maxD <= 2 * kMaxSlots)  // NEXT #3: wide bands, two or four warps per pair
+      rc = tr ? launch_align_wide<2, true>(ctx, A, st, &grid) : launch_align_wide<2, false>(ctx, A, st, &grid);
+    else rc = tr ? launch_align_wide<4, true>(ctx, A, st, &grid) : launch_align_wide<4, false>(ctx, A, st, &grid);
   }
   ctx->stats.packed16 = k16 ? 1 : 0;
   if (rc) {
@@ -1416,6 +1707,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   cudaEventElapsedTime(&ctx->stats.align_ms, ctx->ev[2], ctx->ev[3]);
   cudaEventElapsedTime(&ctx->stats.d2h_ms, ctx->ev[3], ctx->ev[4]);
   ctx->stats.slots_per_lane = K;
+  ctx->stats.warps_per_pair = k16 || maxD <= kMaxSlots ? 1 : (maxD <= 2 * kMaxSlots ? 2 : 4);
   ctx->stats.grid_blocks = grid;
   ctx->stats.kernel_launches = launches;
   ctx->stats.library_launches = lib_launches;

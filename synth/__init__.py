@@ -128,6 +128,15 @@ for _pct in (1, 5, 10, 25, 50):
         Scoring(band_left=500, band_right=500, zdrop=400), lo2=4096, hi2=4096, p_long=_pct / 100,
         description=f"100k pairs, {_pct}% 4096 bp + {100 - _pct}% 128 bp (PAPER.md l.786-788)")
 
+# NEXT #3: wide bands, the C2 recipe with w = 1000 (two warps per pair)
+# and w = 2000 (four warps per pair).
+CONFIGS["CW1"] = dataclasses.replace(CONFIGS["C2"], name="CW1", n_pairs=20_000, seed=201,
+                                     scoring=Scoring(band_left=1000, band_right=1000, zdrop=400),
+                                     description="20k HiFi-like pairs 10-20 kbp, 1% error, w=1000, Z=400")
+CONFIGS["CW2"] = dataclasses.replace(CONFIGS["C2"], name="CW2", n_pairs=10_000, seed=202,
+                                     scoring=Scoring(band_left=2000, band_right=2000, zdrop=400),
+                                     description="10k HiFi-like pairs 10-20 kbp, 1% error, w=2000, Z=400")
+
 _lib: Optional[ctypes.CDLL] = None
 
 

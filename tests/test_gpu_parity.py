@@ -274,9 +274,9 @@ def test_error_codes(gpu_lib, ctx):
         with pytest.raises(gpu_lib.AgathaError) as e:
             gpu_lib.align_pairs(ctx, ok, dict(SCORING, **bad))
         assert e.value.code == gpu_lib.EINVAL
-    with pytest.raises(gpu_lib.AgathaError) as e:  # wider than 1024 diagonals
-        gpu_lib.align_pairs(ctx, synth.from_list([("A" * 2000, "A" * 2000)]),
-                            dict(SCORING, band_left=600, band_right=600))
+    with pytest.raises(gpu_lib.AgathaError) as e:  # wider than 4096 diagonals
+        gpu_lib.align_pairs(ctx, synth.from_list([("A" * 5000, "A" * 5000)]),
+                            dict(SCORING, band_left=2048, band_right=2048))
     assert e.value.code == gpu_lib.ERANGE
     with pytest.raises(gpu_lib.AgathaError) as e:  # penalty beyond the int8 score table
         gpu_lib.align_pairs(ctx, ok, dict(SCORING, mismatch=200))
@@ -300,3 +300,60 @@ def test_variants_random_and_c1(gpu_lib, ctx, kflags, variant):
     cfg = synth.CONFIGS["C1"]
     compare(gpu_lib, ctx, synth.generate(cfg, 0, 300), dict(vars(cfg.scoring), variant=variant),
             flags=kflags)
+
+
+# NEXT #3, the wide-band tier: bands of more than 1024 diagonals run the 32-bit kernel
+# with two (D <= 2048) or four (D <= 4096) warps per pair (DESIGN.md §6.1 "Wide bands").
+@pytest.mark.parametrize("bl,br,warps", [(512, 512, 2), (700, 400, 2), (1023, 1024, 2),
+                                         (1024, 1024, 4), (1500, 900, 4), (2047, 2048, 4),
+                                         (0, 1100, 2), (3000, 1000, 4)])
+def test_wide_bands(gpu_lib, ctx, bl, br, warps):
+    rng = np.random.default_rng(9000 + bl + 7 * br)
+    lst = []
+    for k in range(24):
+        m = int(rng.integers(1500, 4500))
+        a = "".join("ACGT"[x] for x in rng.integers(0, 4, m))
+        q = list(a)
+        for t in range(len(q)):
+            if rng.random() < 0.05:
+                q[t] = "ACGT"[int(rng.integers(0, 4))]
+        q = "".join(q)
+        if k % 4 == 1:  # a long indel: the optimum leaves the main diagonal by hundreds
+            x = int(rng.integers(200, 800))
+            q = q[:x] + q[x + int(rng.integers(200, 900)):]
+        if k % 4 == 2:
+            x = int(rng.integers(200, 800))
+            q = q[:x] + "".join("ACGT"[y] for y in rng.integers(0, 4, int(rng.integers(200, 900)))) + q[x:]
+        if k % 4 == 3:  # chimeric tail (Z-drop)
+            x = int(rng.integers(500, len(q)))
+            q = q[:x] + "".join("ACGT"[y] for y in rng.integers(0, 4, len(q) - x))
+        lst.append((a, q))
+    lst += [("ACGT" * 600, "A"), ("A", "ACGT" * 700), ("N" * 1500, "N" * 2600)]
+    pairs = synth.from_list(lst)
+    for z in (-1, 150):
+        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=bl, band_right=br, zdrop=z))
+        st = ctx.stats()
+        # the widest band actually used decides the tier
+        assert st["packed16"] == 0 and st["warps_per_pair"] == warps, st
+
+
+def test_wide_band_trace(gpu_lib, ctx):
+    """Eq. 5 trace of one pair through the four-warp tier equals the oracle's."""
+    rng = np.random.default_rng(77)
+    a = "".join("ACGT"[x] for x in rng.integers(0, 4, 3000))
+    q = a[:1400] + a[1800:] + "".join("ACGT"[x] for x in rng.integers(0, 4, 300))
+    pairs = synth.from_list([(a, q), (a[:2000], a[100:2500])])
+    params = dict(SCORING, band_left=1600, band_right=1700, zdrop=200)
+    for k in range(pairs.n_pairs):
+        R, Q = pairs.pair(k)
+        cap = len(R) + len(Q) + 1
+        gs, gi = gpu_lib.localmax_trace(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off,
+                                        params, k, cap)
+        assert ctx.stats()["warps_per_pair"] == 4
+        rc, res, (os_, oi) = oracle.align_one(R, Q, params, trace=True)
+        assert rc == 0
+        c_end = res[3] if res[3] >= 0 else len(R) + len(Q)
+        reached = np.arange(cap) <= c_end
+        assert np.array_equal(gi[reached], oi[reached]), k
+        nonempty = reached & (oi >= 0)
+        assert np.array_equal(gs[nonempty], os_[nonempty]), k
