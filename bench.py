@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample stride (0: auto)")
     ap.add_argument("--order", default="lpt", choices=["lpt", "input"])
+    ap.add_argument("--balance", default="static", choices=["static", "dynamic"],
+                    help="static: fixed per-rank shards; dynamic: every rank holds the whole "
+                         "batch and the persistent kernels claim pairs from one counter in "
+                         "rank 0's HBM with system-scope atomics (NEXT #1)")
     return ap.parse_args()
 
 
@@ -205,23 +209,50 @@ def main():
         return (torch.empty(nr, dtype=torch.uint8, pin_memory=True).numpy(),
                 torch.empty(nq, dtype=torch.uint8, pin_memory=True).numpy())
 
+    dynamic = args.balance == "dynamic"
     t0 = time.perf_counter()
-    k0, k1 = adist.shard_range(n, rank)
+    # static: rank r holds its shard; dynamic: every rank holds the whole batch (replicated
+    # inputs) and claims chunks of it at run time
+    k0, k1 = (0, n * world) if dynamic else adist.shard_range(n, rank)
     pairs = synth.generate(full, k0, k1, pinned_out=pinned)
     gen_s = time.perf_counter() - t0
     params = dict(vars(cfg.scoring))
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     d_ref, d_qry = dev(pairs.ref), dev(pairs.qry)
     d_roff, d_qoff = dev(pairs.ref_off.view(np.int64)), dev(pairs.qry_off.view(np.int64))
-    d_out = torch.zeros(adist.RECORD_BYTES * n, dtype=torch.uint8, device="cuda")
+    n_local = k1 - k0
+    d_out = torch.zeros(adist.RECORD_BYTES * n_local, dtype=torch.uint8, device="cuda")
     flags = agatha.ORDER_INPUT if args.order == "input" else 0
     ctx = agatha.Context(local)
     stream = torch.cuda.current_stream()
+    queue = None
+    if dynamic:  # NEXT #1: one pair counter in rank 0's HBM, mapped by every rank
+        if rank == 0:
+            queue = agatha.SharedQueue.create(ctx)
+        handle = adist.share_queue_handle(queue.handle if rank == 0 else b"", world)
+        if rank != 0:
+            queue = agatha.SharedQueue.open(ctx, handle)
+    state = {"kernel_ms": 0.0, "launches": 0}
+
+    def start_dynamic():
+        if rank == 0:
+            queue.reset(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
 
     def step():
+        if dynamic:
+            start_dynamic()
         agatha.align_batch(ctx, d_ref, d_roff, d_qry, d_qoff, params, out=d_out, flags=flags,
-                           stream=stream)
-        if world > 1:
+                           stream=stream, queue=queue)
+        state["kernel_ms"] = ctx.stats()["align_ms"]
+        state["launches"] += ctx.stats()["kernel_launches"]
+        if dynamic:
+            # cells of the pairs this rank claimed (record word 2 = int64 cells), on device
+            state["mine"] = d_out.view(torch.int64).view(-1, 3)[:, 2].sum()
+            adist.merge_claimed(d_out, world)  # NCCL all_reduce of the claimed rows
+        elif world > 1:
             adist.gather_results(d_out, world)  # NCCL all_gather of the 24-byte records
 
     def barrier():
@@ -237,17 +268,22 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
+        state["launches"] = 0
         for _ in range(args.steps):
             step()
-            align_ms.append(ctx.stats()["align_ms"])
+            align_ms.append(state["kernel_ms"])
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
     stats = ctx.stats()
     res = agatha.device_results(d_out)
-    cells_rank = int(res["cells"].sum())
     ms_max = adist.max_over_ranks(ms, "cuda", world)
-    cells_all = adist.sum_over_ranks(float(cells_rank), "cuda", world)
+    if dynamic:  # res is the merged whole batch; this rank aligned the pairs it claimed
+        cells_all = float(res["cells"].sum())
+        cells_rank = int(state["mine"].item())
+    else:
+        cells_rank = int(res["cells"].sum())
+        cells_all = adist.sum_over_ranks(float(cells_rank), "cuda", world)
     sec = ms_max / 1e3
     gcups = cells_all * args.steps / sec / 1e9
     aln_s = n * world * args.steps / sec
@@ -255,15 +291,23 @@ def main():
     # e2e: the public C ABI with pinned host buffers (H2D of inputs + D2H of results each step)
     e2e = None
     if not args.no_e2e:
-        host_out = np.zeros(n, agatha.RESULT_DTYPE)
-        for _ in range(1):
+        host_out = np.zeros(n_local, agatha.RESULT_DTYPE)
+
+        def e2e_step():
+            if dynamic:
+                start_dynamic()
             agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
-                               out=host_out, flags=flags, stream=stream)
+                               out=host_out, flags=flags, stream=stream, queue=queue)
+            if dynamic and world > 1:  # merge the ranks' claimed rows
+                t = torch.from_numpy(host_out.view(np.uint8)).cuda()
+                adist.merge_claimed(t, world)
+                host_out.view(np.uint8)[:] = t.cpu().numpy()
+
+        e2e_step()
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
-                               out=host_out, flags=flags, stream=stream)
+            e2e_step()
         ev1.record(stream)
         barrier()
         e_ms = adist.max_over_ranks(ev0.elapsed_time(ev1), "cuda", world)
@@ -271,7 +315,7 @@ def main():
         h2d = int(pairs.ref.nbytes + pairs.qry.nbytes + pairs.ref_off.nbytes + pairs.qry_off.nbytes)
         e2e = {"value": cells_all * args.steps / (e_ms / 1e3) / 1e9, "unit": "GCUPS",
                "alignments_per_s": n * world * args.steps / (e_ms / 1e3),
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 24 * n,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 24 * n_local,
                "ms_per_step": e_ms / args.steps}
 
     if rank != 0:
@@ -318,10 +362,14 @@ def main():
         "metric": "GCUPS", "value": gcups, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": config_dict(cfg, n, world), "alignments_per_s": aln_s,
+        "config": dict(config_dict(cfg, n, world), balance=args.balance,
+                       parallelism=(f"{world} GPU(s) claim pairs from one shared counter "
+                                    "(system-scope atomics, NEXT #1)") if dynamic
+                       else f"pairs sharded over {world} GPU(s)"),
+        "alignments_per_s": aln_s,
         "cells_per_step": cells_all, "zdrop_terminated": int((res["zdrop_antidiag"] >= 0).sum()),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": stats["kernel_launches"] * args.steps,
+        "gpu_launches": state["launches"],
         "library_launches": stats["library_launches"] * args.steps,
         "stats_last_step": stats, "clocks": clocks, "parity": parity,
         "gen_seconds": gen_s,

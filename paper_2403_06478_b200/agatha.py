@@ -47,7 +47,7 @@ VAR_GATE_GE, VAR_ORIGIN_MAX, VAR_CHECK_LAST = 1, 2, 4
 class Batch(ctypes.Structure):
     _fields_ = [("ref", ctypes.c_void_p), ("qry", ctypes.c_void_p), ("ref_off", ctypes.c_void_p),
                 ("qry_off", ctypes.c_void_p), ("n_pairs", ctypes.c_uint64),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("queue", ctypes.c_void_p)]
 
 
 class Stats(ctypes.Structure):
@@ -78,6 +78,10 @@ def _load() -> ctypes.CDLL:
     lib.agatha_strerror.argtypes = [ctypes.c_int]
     lib.agatha_strerror.restype = ctypes.c_char_p
     lib.agatha_version.restype = ctypes.c_int
+    lib.agatha_queue_create.argtypes = [vp, ctypes.POINTER(vp), ctypes.c_char_p]
+    lib.agatha_queue_open.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(vp)]
+    lib.agatha_queue_reset.argtypes = [vp, vp, vp]
+    lib.agatha_queue_close.argtypes = [vp, vp, ctypes.c_int]
     return lib
 
 
@@ -86,7 +90,8 @@ _lib = _load()
 # Every symbol include/agatha.h declares (checked by tests/test_abi.py).
 EXPORTS = ("agatha_ctx_create", "agatha_ctx_destroy", "agatha_align_batch", "agatha_pack4",
            "agatha_plan", "agatha_localmax_trace", "agatha_get_stats", "agatha_strerror",
-           "agatha_version")
+           "agatha_version", "agatha_queue_create", "agatha_queue_open", "agatha_queue_reset",
+           "agatha_queue_close")
 
 
 def lib() -> ctypes.CDLL:
@@ -164,6 +169,44 @@ class Context:
         return s.as_dict()
 
 
+class SharedQueue:
+    """A pair counter shared by several contexts, processes or GPUs (agatha_queue_*;
+    cross-GPU dynamic balancing, NEXT #1).  ``SharedQueue.create(ctx)`` allocates it and
+    exposes ``handle`` (64 bytes, to send to the other participants);
+    ``SharedQueue.open(ctx, handle)`` maps one created by another process.  Pass
+    ``queue=`` to align_batch."""
+
+    def __init__(self, ctx: Context, ptr: int, handle: bytes, opened: bool):
+        self.ctx, self.ptr, self.handle, self.opened = ctx, ptr, handle, opened
+
+    @classmethod
+    def create(cls, ctx: Context) -> "SharedQueue":
+        q = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(64)
+        rc = _lib.agatha_queue_create(ctx.handle, ctypes.byref(q), h)
+        if rc != OK:
+            raise AgathaError(rc, "agatha_queue_create")
+        return cls(ctx, int(q.value), h.raw, False)
+
+    @classmethod
+    def open(cls, ctx: Context, handle: bytes) -> "SharedQueue":
+        q = ctypes.c_void_p()
+        rc = _lib.agatha_queue_open(ctx.handle, bytes(handle), ctypes.byref(q))
+        if rc != OK:
+            raise AgathaError(rc, "agatha_queue_open")
+        return cls(ctx, int(q.value), bytes(handle), True)
+
+    def reset(self, stream=None):
+        rc = _lib.agatha_queue_reset(self.ctx.handle, self.ptr, _stream_ptr(stream))
+        if rc != OK:
+            raise AgathaError(rc, "agatha_queue_reset")
+
+    def close(self):
+        if self.ptr:
+            _lib.agatha_queue_close(self.ctx.handle, self.ptr, int(self.opened))
+            self.ptr = 0
+
+
 def _ptr(a) -> int:
     if a is None:
         return 0
@@ -188,10 +231,14 @@ def make_batch(ref, ref_off, qry, qry_off, flags: int = 0) -> Batch:
 
 
 def align_batch(ctx: Context, ref, ref_off, qry, qry_off, params, out=None, flags: int = 0,
-                stream=None):
+                stream=None, queue: Optional["SharedQueue"] = None):
     """agatha_align_batch.  Returns ``out`` (a numpy RESULT_DTYPE array for host outputs,
-    or the given CUDA uint8/int tensor of 24*n_pairs bytes for device outputs)."""
+    or the given CUDA uint8/int tensor of 24*n_pairs bytes for device outputs).  With a
+    ``queue`` (SharedQueue) only the pairs this call claims are aligned; the other rows of
+    ``out`` are zero."""
     b = make_batch(ref, ref_off, qry, qry_off, flags)
+    if queue is not None:
+        b.queue = queue.ptr
     p = params_from(params)
     if out is None:
         out = np.zeros(b.n_pairs, RESULT_DTYPE)
@@ -208,6 +255,12 @@ def align_pairs(ctx: Context, pairs, params, flags: int = 0, stream=None):
     """Convenience: align a ``synth.Pairs``-like object (host arrays)."""
     return align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
                        flags=flags, stream=stream)
+
+
+def align_pairs_q(ctx: Context, pairs, params, out, queue: "SharedQueue", stream=None, flags: int = 0):
+    """align_pairs into ``out`` claiming pairs from a SharedQueue (NEXT #1)."""
+    return align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params, out=out,
+                       flags=flags, stream=stream, queue=queue)
 
 
 def device_results(out_tensor):

@@ -64,6 +64,7 @@ struct AlignArgs {
   const uint8_t* bad;        // per-pair validation flag from the prep kernel
   agatha_result_t* out;
   int* queue;                // global work counter (a7)
+  int sysq;                  // 1: the counter is shared across GPUs/processes (system scope)
   uint32_t n_pairs;
   int bl, br;                // band; negative = unbounded
   int alpha, beta, zdrop;
@@ -80,6 +81,12 @@ struct AlignArgs {
   int ref16;                 // 16-bit kernel: stored value of the anti-diagonal max after
                              // a re-centring (negative)
 };
+
+// a7: the next position of the dispatch order.  A shared counter (NEXT #1) lives in
+// another GPU's or process's memory, so it is claimed with a system-scope atomic.
+__device__ __forceinline__ int claim_next(const AlignArgs& A) {
+  return A.sysq ? atomicAdd_system(A.queue, 1) : atomicAdd(A.queue, 1);
+}
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
@@ -471,7 +478,7 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignAr
   const int lane = threadIdx.x & 31;
   for (;;) {
     int q = 0;
-    if (lane == 0) q = atomicAdd(A.queue, 1);
+    if (lane == 0) q = claim_next(A);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
     align_pair<K, TRACE>(A, A.order[q], lane);
@@ -731,7 +738,7 @@ __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A)
   __shared__ WideShared sh;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (;;) {
-    if (threadIdx.x == 0) sh.q = atomicAdd(A.queue, 1);
+    if (threadIdx.x == 0) sh.q = claim_next(A);
     __syncthreads();
     const int q = sh.q;
     __syncthreads();  // every thread has read q before thread 0 takes the next one
@@ -1243,7 +1250,7 @@ __global__ void __launch_bounds__(128, NREG >= 16 ? 3 : 4) align16_kernel(AlignA
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (;;) {
     int q = 0;
-    if (lane == 0) q = atomicAdd(A.queue, 1);
+    if (lane == 0) q = claim_next(A);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
     align_pair16<NREG, TRACE, NCAP>(A, A.order[q], lane, snap_all[warp]);
@@ -1640,7 +1647,11 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   A.ref_ascii = d_ref; A.qry_ascii = d_qry; A.chunk_of = (const uint8_t*)ctx->chunk_of.p;
   A.ready = d_ready; A.err_flags = d_sc; A.nmap = nmap ? 1 : 0;
   A.roff = d_roff; A.qoff = d_qoff; A.order = d_order; A.bad = (const uint8_t*)ctx->bad.p;
-  A.out = d_out; A.queue = d_sc + 2; A.n_pairs = (uint32_t)P;
+  A.out = d_out; A.n_pairs = (uint32_t)P;
+  A.queue = b->queue ? b->queue : d_sc + 2;  // NEXT #1: a counter shared with other GPUs
+  A.sysq = b->queue ? 1 : 0;
+  if (b->queue)  // rows this participant does not claim stay zero (merged by the caller)
+    CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(agatha_result_t) * P, st));
   A.bl = p->band_left; A.br = p->band_right;
   A.alpha = p->gap_open; A.beta = p->gap_extend; A.zdrop = p->zdrop; A.sixteen = 16;
   A.variant = p->variant;
@@ -1798,6 +1809,7 @@ int agatha_localmax_trace(agatha_ctx_t* ctx, const agatha_batch_t* batch, const 
   CUDA_TRY(cudaMemsetAsync(ti, 0xff, 4 * (size_t)cap, st));
   agatha_batch_t b2 = *batch;
   b2.flags |= AGATHA_OUT_DEVICE;
+  b2.queue = nullptr;  // the traced pair must run on this context
   rc = run_batch(ctx, &b2, params, tout, st, (long long)pair, ts, ti, cap);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(score, ts, 4 * (size_t)cap, cudaMemcpyDeviceToHost, st));
@@ -1872,6 +1884,53 @@ int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* b, const agatha_params_
 int agatha_get_stats(const agatha_ctx_t* ctx, agatha_stats_t* stats) {
   if (!ctx || !stats) return AGATHA_EINVAL;
   *stats = ctx->stats;
+  return AGATHA_OK;
+}
+
+// NEXT #1: shared pair counters (cross-GPU / cross-process dynamic balancing).
+int agatha_queue_create(agatha_ctx_t* ctx, int32_t** queue, uint8_t handle[64]) {
+  if (!ctx || !queue || !handle) return AGATHA_EINVAL;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  int32_t* q = nullptr;
+  if (cudaMalloc(&q, 256) != cudaSuccess) {
+    cudaGetLastError();
+    return AGATHA_ENOMEM;
+  }
+  CUDA_TRY(cudaMemset(q, 0, 256));
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+  if (cudaIpcGetMemHandle(&h, q) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(q);
+    return AGATHA_ECUDA;
+  }
+  memcpy(handle, &h, 64);
+  *queue = q;
+  return AGATHA_OK;
+}
+
+int agatha_queue_open(agatha_ctx_t* ctx, const uint8_t handle[64], int32_t** queue) {
+  if (!ctx || !queue || !handle) return AGATHA_EINVAL;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *queue = (int32_t*)p;
+  return AGATHA_OK;
+}
+
+int agatha_queue_reset(agatha_ctx_t* ctx, int32_t* queue, void* stream) {
+  if (!ctx || !queue) return AGATHA_EINVAL;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(cudaMemsetAsync(queue, 0, sizeof(int32_t), (cudaStream_t)stream));
+  return AGATHA_OK;
+}
+
+int agatha_queue_close(agatha_ctx_t* ctx, int32_t* queue, int opened) {
+  if (!ctx || !queue) return AGATHA_EINVAL;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(opened ? cudaIpcCloseMemHandle(queue) : cudaFree(queue));
   return AGATHA_OK;
 }
 

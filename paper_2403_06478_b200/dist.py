@@ -1,5 +1,11 @@
 """Multi-GPU plumbing: pairs shard across ranks; NCCL only gathers results.
 
+Two ways to split a batch: fixed contiguous shards (shard_range / split_range, the
+default) or cross-GPU dynamic balancing (NEXT #1): every rank holds the whole batch and
+its persistent kernel claims pairs from one counter in rank 0's HBM with system-scope
+atomics (agatha_queue_*, handle exchanged by share_queue_handle); each rank's output has
+only its own rows, merged by merge_claimed.
+
 The path has no data exchange between pairs (§5.8 l.843-846: independent
 per-GPU processing), so each rank aligns its own shard and the only collective is the
 gather of the fixed 24-byte result records (BASELINE.json north_star: "NCCL over
@@ -25,6 +31,30 @@ def split_range(n_pairs: int, world: int, rank: int) -> Tuple[int, int]:
     base, extra = divmod(n_pairs, world)
     k0 = rank * base + min(rank, extra)
     return k0, k0 + base + (1 if rank < extra else 0)
+
+
+def share_queue_handle(handle: bytes, world: int, src: int = 0) -> bytes:
+    """Broadcast the 64-byte CUDA IPC handle of rank src's shared pair counter
+    (agatha_queue_create) to every rank; the others map it with agatha_queue_open."""
+    import torch.distributed as dist
+
+    if world == 1:
+        return handle
+    box = [handle]
+    dist.broadcast_object_list(box, src=src)
+    return bytes(box[0])
+
+
+def merge_claimed(records, world: int, group=None):
+    """Merge per-rank result buffers in which each rank filled only the rows it claimed
+    (all other rows zero): an all_reduce(SUM) over the records viewed as int64 words, which
+    is exact because every row is non-zero on at most one rank."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.all_reduce(records.view(-1).view(torch.int64), op=dist.ReduceOp.SUM, group=group)
+    return records
 
 
 def gather_results(local, world: int, group=None):

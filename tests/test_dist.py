@@ -82,3 +82,35 @@ def test_gloo_world2_gather(tmp_path):
     assert gathered.tobytes() == exp.tobytes()
     assert tmax == 2.0
     assert tsum == float(exp["cells"].sum())
+
+
+def _merge_worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.CONFIGS["C1"]
+    n = N_PER_RANK * world
+    pairs = synth.generate(cfg.with_pairs(n), 0, n)  # replicated inputs
+    rc, res, _ = oracle.align_batch(pairs, vars(cfg.scoring), threads=1)
+    assert rc == 0
+    # this rank "claimed" every other pair (as a shared device counter would interleave)
+    mine = res.copy()
+    mine[(np.arange(n) % world) != rank] = np.zeros(1, oracle.RESULT_DTYPE)
+    records = torch.from_numpy(mine.view(np.uint8).copy())
+    adist.merge_claimed(records, world)
+    handle = adist.share_queue_handle(bytes(range(64)) if rank == 0 else b"", world)
+    if rank == 0:
+        np.save(os.path.join(outdir, "merged.npy"), records.numpy())
+        np.save(os.path.join(outdir, "expected.npy"), res.view(np.uint8))
+    assert handle == bytes(range(64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_dynamic_merge(tmp_path):
+    """NEXT #1 plumbing: the queue handle reaches every rank, and the all-reduce of the
+    ranks' claimed rows reproduces the whole batch."""
+    world = 2
+    mp.spawn(_merge_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    assert np.load(tmp_path / "merged.npy").tobytes() == np.load(tmp_path / "expected.npy").tobytes()

@@ -357,3 +357,85 @@ def test_wide_band_trace(gpu_lib, ctx):
         assert np.array_equal(gi[reached], oi[reached]), k
         nonempty = reached & (oi >= 0)
         assert np.array_equal(gs[nonempty], os_[nonempty]), k
+
+
+# NEXT #1, cross-GPU dynamic balancing: participants that share one pair counter align
+# disjoint subsets of the same batch, and their merged rows equal a one-context run.
+def _merge_rows(*outs):
+    acc = np.zeros(len(outs[0]) * 3, np.int64)
+    for o in outs:
+        acc += o.view(np.int64)
+    return acc.view(oracle.RESULT_DTYPE)
+
+
+def test_shared_queue_two_contexts(gpu_lib, ctx):
+    import threading
+    cfg = synth.CONFIGS["C5"]
+    pairs = synth.generate(cfg, 0, 600)
+    params = vars(cfg.scoring)
+    full = gpu_lib.align_pairs(ctx, pairs, params)
+    c2 = gpu_lib.Context(0)
+    q = gpu_lib.SharedQueue.create(ctx)
+    try:
+        for rep in range(3):
+            q.reset()
+            import torch
+            torch.cuda.synchronize()
+            outs = [np.zeros(pairs.n_pairs, gpu_lib.RESULT_DTYPE) for _ in range(2)]
+
+            def run(k, c):
+                s = torch.cuda.Stream()
+                gpu_lib.align_pairs_q(c, pairs, params, outs[k], q, s)
+
+            th = [threading.Thread(target=run, args=(k, c)) for k, c in enumerate((ctx, c2))]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            claimed = [int((o["cells"] != 0).sum()) for o in outs]
+            assert sum(claimed) == pairs.n_pairs, claimed
+            assert _merge_rows(*outs).tobytes() == full.tobytes()
+    finally:
+        q.close()
+        c2.close()
+
+
+def _ipc_worker(rank, handle_q, result_q):
+    import torch
+    from paper_2403_06478_b200 import agatha
+    torch.cuda.set_device(0)
+    c = agatha.Context(0)
+    cfg = synth.CONFIGS["C5"]
+    pairs = synth.generate(cfg, 0, 400)
+    if rank == 0:
+        q = agatha.SharedQueue.create(c)
+        handle_q.put(q.handle)
+    else:
+        q = agatha.SharedQueue.open(c, handle_q.get())
+    out = np.zeros(pairs.n_pairs, agatha.RESULT_DTYPE)
+    result_q.put(("ready", rank))
+    agatha.align_batch(c, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, vars(cfg.scoring),
+                       out=out, queue=q)
+    result_q.put((rank, out.tobytes()))
+
+
+def test_shared_queue_two_processes(gpu_lib, ctx):
+    """The counter crosses processes through its CUDA IPC handle (agatha_queue_open),
+    as it would cross GPUs; claims use system-scope atomics."""
+    import torch.multiprocessing as tmp
+    mpc = tmp.get_context("spawn")
+    hq, rq = mpc.Queue(), mpc.Queue()
+    ps = [mpc.Process(target=_ipc_worker, args=(r, hq, rq)) for r in range(2)]
+    for p_ in ps:
+        p_.start()
+    got = {}
+    while len(got) < 2:
+        item = rq.get(timeout=300)
+        if item[0] != "ready":
+            got[item[0]] = np.frombuffer(item[1], gpu_lib.RESULT_DTYPE)
+    for p_ in ps:
+        p_.join(timeout=120)
+    cfg = synth.CONFIGS["C5"]
+    pairs = synth.generate(cfg, 0, 400)
+    full = gpu_lib.align_pairs(ctx, pairs, vars(cfg.scoring))
+    assert _merge_rows(got[0], got[1]).tobytes() == full.tobytes()
