@@ -979,7 +979,7 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
 }
 
 template <int NREG, bool TRACE, int NCAP>
-__device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap) {
+__device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap, uint32_t* pref) {
   constexpr int K = 2 * NREG;        // slots per lane
   constexpr int NC = NREG;           // cells per step per lane (K/2)
   const uint64_t r0 = A.roff[pid], q0 = A.qoff[pid];
@@ -1078,6 +1078,18 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   int wQ = qpos >> 3, oQ = qpos & 7;  // oQ = 7 = 7 - oR from here on
   uint32_t Wq0 = load_word_rw(Qw, wQ, nwQ), Wq1 = load_word_rw(Qw, wQ + 1, nwQ),
            Wq2 = load_word_rw(Qw, wQ + 2, nwQ);
+  // the words the next refill needs are copied global -> shared asynchronously (no
+  // registers held, the load latency hides behind 8 iterations)
+  auto prefetch = [&]() {
+    const uint32_t* gr = Rw + min(max(wR + 3 + 1, 0), nwR + 1);
+    const uint32_t* gq = Qw + min(max(wQ - 1 + 1, 0), nwQ + 1);
+    const unsigned sr = (unsigned)__cvta_generic_to_shared(pref + lane);
+    const unsigned sq = (unsigned)__cvta_generic_to_shared(pref + 32 + lane);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(sr), "l"(gr) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(sq), "l"(gq) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  prefetch();
 
   const uint32_t T0 = A.T16_0, T1 = A.T16_1, k65536 = A.k65536, one = A.one;
   const int ref16 = -s.B;
@@ -1170,10 +1182,12 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     if (oR == 8) {  // oQ == -1 at the same time (phase-aligned packing)
       oR = 0;
       ++wR;
-      Wr0 = Wr1; Wr1 = Wr2; Wr2 = load_word_rw(Rw, wR + 2, nwR);
       oQ = 7;
       --wQ;
-      Wq2 = Wq1; Wq1 = Wq0; Wq0 = load_word_rw(Qw, wQ, nwQ);
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      Wr0 = Wr1; Wr1 = Wr2; Wr2 = pref[lane];
+      Wq2 = Wq1; Wq1 = Wq0; Wq0 = pref[32 + lane];
+      prefetch();
     }
     if (iters >= kRebase16) {  // re-centre: the last anti-diagonal max moves to ref16
       iters = 0;
@@ -1247,13 +1261,14 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 template <int NREG, bool TRACE, int NCAP>
 __global__ void __launch_bounds__(128, NREG >= 16 ? 3 : 4) align16_kernel(AlignArgs A) {
   __shared__ uint32_t snap_all[4][NREG / 2 * 32];
+  __shared__ uint32_t pref_all[4][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (;;) {
     int q = 0;
     if (lane == 0) q = claim_next(A);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
-    align_pair16<NREG, TRACE, NCAP>(A, A.order[q], lane, snap_all[warp]);
+    align_pair16<NREG, TRACE, NCAP>(A, A.order[q], lane, snap_all[warp], pref_all[warp]);
   }
 }
 
