@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample stride (0: auto)")
     ap.add_argument("--order", default="lpt", choices=["lpt", "input"])
+    ap.add_argument("--tiers", default="split", choices=["split", "single"],
+                    help="16-bit kernel: each pair at its own slot tier (default) or one "
+                         "launch at the widest front (ablation; input order implies single)")
     ap.add_argument("--balance", default="static", choices=["static", "dynamic"],
                     help="static: fixed per-rank shards; dynamic: every rank holds the whole "
                          "batch and the persistent kernels claim pairs from one counter in "
@@ -223,6 +226,8 @@ def main():
     n_local = k1 - k0
     d_out = torch.zeros(adist.RECORD_BYTES * n_local, dtype=torch.uint8, device="cuda")
     flags = agatha.ORDER_INPUT if args.order == "input" else 0
+    if args.tiers == "single":
+        flags |= agatha.SINGLE_TIER
     ctx = agatha.Context(local)
     stream = torch.cuda.current_stream()
     queue = None
@@ -332,7 +337,8 @@ def main():
     ops = OPS_PER_CELL if stats.get("packed16") else OPS_PER_CELL_32
     achieved_tops = ops * cells_rank / (align_avg_ms / 1e3) / 1e12
     if stats.get("packed16"):
-        kname = f"align16_kernel<{stats['slots_per_lane'] // 2}>"
+        tiers = [32 >> t for t in range(3) if stats.get("tier_pairs", [1, 0, 0])[t]]
+        kname = " + ".join(f"align16_kernel<{k // 2}>" for k in tiers) or "align16_kernel"
     elif stats.get("warps_per_pair", 1) > 1:
         kname = f"align_wide_kernel<{stats['warps_per_pair']}>"
     else:

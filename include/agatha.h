@@ -52,6 +52,10 @@ extern "C" {
                                      (ordering ablation; results are identical)           */
 #define AGATHA_FORCE_32BIT 32u    /* use the 32-bit kernel even when the 16-bit packed one is
                                      exact for these parameters (results are identical)   */
+#define AGATHA_SINGLE_TIER 64u    /* run every pair of the 16-bit kernel at the front the
+                                     batch's widest band needs, in one launch, instead of
+                                     each pair at the narrowest slot tier that holds its
+                                     band (tier ablation; results are identical)          */
 
 /* Scoring (Eq. 1-4 symbols).  Penalties are POSITIVE numbers. */
 typedef struct {
@@ -117,6 +121,8 @@ typedef struct {
   int32_t library_launches; /* CUB radix-sort kernels launched by the call             */
   int32_t packed16;    /* 1 if the 16-bit packed (DPX .S16x2) kernel ran, 0 for 32-bit    */
   int32_t warps_per_pair; /* 1; 2 or 4 in the wide-band tier (D > 1024, 32-bit)          */
+  int32_t tier_pairs[3]; /* 16-bit kernel: pairs run at 32 / 16 / 8 slots per lane (the
+                            slot tiers for D > 512 / 257..512 / <= 256 diagonals)         */
 } agatha_stats_t;
 
 /* Create a context on CUDA device `cuda_device`.  Fails with AGATHA_ECUDA when the

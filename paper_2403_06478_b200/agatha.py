@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_PKG, "libagatha.so")
 
 OK, EINVAL, EEMPTY, ECHAR, ERANGE, ECUDA, ENOMEM = 0, -1, -2, -3, -4, -5, -6
 MEM_HOST, MEM_DEVICE, OUT_DEVICE = 0, 1, 2
-N_REJECT, N_MAP, PACK_REVERSE, ORDER_INPUT, FORCE_32BIT = 0, 4, 8, 16, 32
+N_REJECT, N_MAP, PACK_REVERSE, ORDER_INPUT, FORCE_32BIT, SINGLE_TIER = 0, 4, 8, 16, 32, 64
 
 RESULT_DTYPE = np.dtype([("score", "<i4"), ("ref_end", "<i4"), ("query_end", "<i4"),
                          ("zdrop_antidiag", "<i4"), ("cells", "<i8")])
@@ -55,10 +55,12 @@ class Stats(ctypes.Structure):
                 ("align_ms", ctypes.c_float), ("d2h_ms", ctypes.c_float),
                 ("slots_per_lane", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
                 ("kernel_launches", ctypes.c_int32), ("library_launches", ctypes.c_int32),
-                ("packed16", ctypes.c_int32), ("warps_per_pair", ctypes.c_int32)]
+                ("packed16", ctypes.c_int32), ("warps_per_pair", ctypes.c_int32),
+                ("tier_pairs", ctypes.c_int32 * 3)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        return {k: (list(v) if k == "tier_pairs" else v)
+                for k, v in ((k, getattr(self, k)) for k, _ in self._fields_)}
 
 
 def _load() -> ctypes.CDLL:

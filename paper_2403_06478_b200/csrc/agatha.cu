@@ -1109,13 +1109,21 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         const uint32_t b = (uint32_t)(k & 3);
         S2[k] = prmt(k < 4 ? a0 : a1, k < 4 ? b0 : b1, b | ((b | 8) << 4) | ((4 + b) << 8) | (((4 + b) | 8) << 12));
       }
-    } else {  // NREG == 8: cells 0..7 in one word, pairs (t, t+4)
+    } else if (NREG == 8) {  // cells 0..7 in one word, pairs (t, t+4)
       const uint32_t x0 = combine(__funnelshift_rc(Wr[0], Wr[1], shiftR), qg[0]);
       const uint32_t a0 = prmt(T0, T1, x0), a1 = prmt(T0, T1, shr16_fma(x0, k65536));
 #pragma unroll
       for (int k = 0; k < NREG / 2; ++k) {
         const uint32_t b = (uint32_t)k;
         S2[k] = prmt(a0, a1, b | ((b | 8) << 4) | ((4 + b) << 8) | (((4 + b) | 8) << 12));
+      }
+    } else {  // NREG == 4 (narrow tier): cells 0..3 from the low half-word, pairs (t, t+2)
+      const uint32_t x0 = combine(__funnelshift_rc(Wr[0], Wr[1], shiftR), qg[0]);
+      const uint32_t a0 = prmt(T0, T1, x0);
+#pragma unroll
+      for (int k = 0; k < NREG / 2; ++k) {
+        const uint32_t b = (uint32_t)k;
+        S2[k] = prmt(a0, 0u, b | ((b | 8) << 4) | ((2 + b) << 8) | (((2 + b) | 8) << 12));
       }
     }
   };
@@ -1209,11 +1217,17 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     }
   };
   // run `total` iterations of one phase
+  int ph = 0;  // iterations so far (mod 8): lane-uniform, unlike oR when NC = 4
   auto run_phase = [&](auto masked_tag, int total) {
     while (!stop && total > 0) {
-      int k = 8 - oR;  // iters == oR (mod 8): runs end at refill / re-centring points together
+      // iters == oR (mod 8): runs end at refill / re-centring points together.  With
+      // NC = 4 cells per lane, odd lanes sit half a word (oR = 4) ahead of even lanes, so
+      // runs end every 4 iterations and each lane refills when its own oR reaches 8; the
+      // run length must be lane-uniform (the iterations hold warp shuffles).
+      int k = NC >= 8 ? 8 - oR : 4 - (ph & 3);
       k = min(k, kRebase16 - iters);
       k = min(k, total);
+      ph += k;
       total -= k;
       iters += k;
 #pragma unroll 1
@@ -1259,7 +1273,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 }
 
 template <int NREG, bool TRACE, int NCAP>
-__global__ void __launch_bounds__(128, NREG >= 16 ? 3 : 4) align16_kernel(AlignArgs A) {
+__global__ void __launch_bounds__(128, NREG >= 16 ? 3 : (NREG >= 8 ? 4 : 5)) align16_kernel(AlignArgs A) {
   __shared__ uint32_t snap_all[4][NREG / 2 * 32];
   __shared__ uint32_t pref_all[4][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1300,8 +1314,22 @@ struct PrepArgs {
   const uint64_t* chunk_first;  // nchunks + 1 pair boundaries of the input chunks
   int nchunks;
   uint8_t* chunk_of;            // out: chunk of each pair
-  uint64_t* key64;              // out: dispatch key (chunk << 32) | ~nominal, ascending
+  uint64_t* key64;              // out: dispatch key (tier << tier_shift) | (chunk << 32) | ~nominal,
+                                // ascending: tier-major, chunk-major, longest first
+  int tier_shift;               // 32 + chunk-id bits
+  int* tier_count;              // [3] pairs per slot tier (tier_of)
+  int* max_off16_t0;            // max (-D) mod 16 over the pairs of tier 0
 };
+
+// Slot tier of a pair of the 16-bit kernel (DESIGN.md §6.1 "Slot tiers"): the narrowest
+// of 32 / 16 / 8 slots per lane (NREG 16 / 8 / 4) whose 32-lane front holds its D
+// diagonals.  Tier 0 first in the dispatch key, so the widest pairs start first.
+#ifndef AGATHA_NARROW_TIER
+#define AGATHA_NARROW_TIER 1
+#endif
+__host__ __device__ __forceinline__ int tier_of(int64_t D) {
+  return D > 512 ? 0 : ((D > 256 || !AGATHA_NARROW_TIER) ? 1 : 2);
+}
 
 __global__ void prep_kernel(PrepArgs P) {
   const int lane = threadIdx.x & 31;
@@ -1341,13 +1369,20 @@ __global__ void prep_kernel(PrepArgs P) {
           if (P.chunk_first[mid] <= p) lo = mid; else hi = mid - 1;
         }
         P.chunk_of[p] = (uint8_t)lo;
-        P.key64[p] = ((uint64_t)lo << 32) | (uint64_t)(0xffffffffu - nom);
+        const uint64_t tier = flag ? 0 : (uint64_t)tier_of(D);
+        P.key64[p] = (tier << P.tier_shift) | ((uint64_t)lo << 32) | (uint64_t)(0xffffffffu - nom);
       }
       P.bad[p] = (uint8_t)(flag != 0);
-      if (flag) atomicOr(P.err_flags, flag);
-      else {
+      if (flag) {
+        atomicOr(P.err_flags, flag);
+        if (P.tier_count) atomicAdd(P.tier_count, 1);  // (the call then fails anyway)
+      } else {
         atomicMax(P.max_slots, (int)D);
         atomicMax(P.max_off16, (int)((-D) & 15));
+        if (P.tier_count) {
+          atomicAdd(P.tier_count + tier_of(D), 1);
+          if (tier_of(D) == 0) atomicMax(P.max_off16_t0, (int)((-D) & 15));
+        }
       }
     }
   }
@@ -1381,6 +1416,8 @@ struct agatha_ctx {
   cudaStream_t copy_stream = nullptr;                 // H2D of input chunks
   cudaEvent_t ev[6];
   cudaEvent_t cev[2];
+  cudaStream_t tier_stream[2] = {nullptr, nullptr};  // slot tiers 1 and 2
+  cudaEvent_t tev[3];                                 // fork (0) / joins (1, 2) of the tiers
   agatha_stats_t stats;
 };
 
@@ -1615,9 +1652,11 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     if ((rc = grow(ctx->results, sizeof(agatha_result_t) * P))) return rc;
     d_out = (agatha_result_t*)ctx->results.p;
   }
-  int* d_sc = (int*)ctx->scalars.p;  // [0] err_flags [1] max_slots [2] queue [3] max (-D) mod 16
+  // scalars: [0] err_flags [1] max_slots [2] queue (tier 0 / one launch) [3] max (-D) mod 16
+  // [4..6] pairs per slot tier [7] max (-D) mod 16 of tier 0 [8] [9] queues of tiers 1, 2
+  int* d_sc = (int*)ctx->scalars.p;
   int* d_ready = (int*)ctx->ready.p;
-  CUDA_TRY(cudaMemsetAsync(d_sc, 0, 16, st));
+  CUDA_TRY(cudaMemsetAsync(d_sc, 0, 40, st));
   CUDA_TRY(cudaMemcpyAsync(ctx->chunk_first.p, ctx->h_chunk_first, 8 * (nchunks + 1),
                            cudaMemcpyHostToDevice, st));
   if (dev_in) CUDA_TRY(cudaMemcpyAsync(d_ready, ctx->h_ones, 4, cudaMemcpyHostToDevice, st));
@@ -1633,15 +1672,18 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1; pa.max_off16 = d_sc + 3;
   pa.chunk_first = (const uint64_t*)ctx->chunk_first.p; pa.nchunks = nchunks;
   pa.chunk_of = (uint8_t*)ctx->chunk_of.p; pa.key64 = (uint64_t*)ctx->key64.p;
+  int chunk_bits = 0;
+  while ((1 << chunk_bits) < nchunks) ++chunk_bits;
+  pa.tier_shift = 32 + chunk_bits; pa.tier_count = d_sc + 4; pa.max_off16_t0 = d_sc + 7;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
   CUDA_TRY(cudaGetLastError());
   int launches = 1, lib_launches = 0;
   const uint32_t* d_order = (const uint32_t*)ctx->iota.p;
   if (!(b->flags & AGATHA_ORDER_INPUT)) {
-    // a2: longest first within each input chunk (chunk-major): key = (chunk << 32) | ~nominal
-    int end_bit = 32;
-    while ((1 << (end_bit - 32)) < nchunks) ++end_bit;
+    // a2: longest first within each input chunk (chunk-major) within each slot tier
+    // (tier-major): key = (tier << (32 + chunk_bits)) | (chunk << 32) | ~nominal
+    const int end_bit = 32 + chunk_bits + 2;
     size_t tb = ctx->sort_tmp.cap;
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(
         ctx->sort_tmp.p, tb, (const uint64_t*)ctx->key64.p, (uint64_t*)ctx->key64_sorted.p,
@@ -1650,9 +1692,11 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     lib_launches = 4;
   }
   // K (slots per lane) from the widest band in the batch
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 16, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 40, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   const int err0 = ctx->h_scalars[0], maxD = ctx->h_scalars[1], maxoff16 = ctx->h_scalars[3];
+  const int tier_n[3] = {ctx->h_scalars[4], ctx->h_scalars[5], ctx->h_scalars[6]};
+  const int maxoff16_t0 = ctx->h_scalars[7];
   if (err0 & 2) return AGATHA_EEMPTY;
   if (err0 & 4) return AGATHA_ERANGE;
   CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
@@ -1699,26 +1743,69 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   const int K = maxD <= 512 ? 16 : 32;
   const bool k16 = use16(p, maxD) && !(b->flags & AGATHA_FORCE_32BIT);
   const bool tr = trace_pair >= 0;
-  if (k16) {
+  // Slot tiers: each pair runs at the narrowest front that holds its
+  // band, one persistent launch per non-empty tier on its own stream, so the narrow
+  // tiers fill the SMs as the wide tier's blocks retire.  The order is tier-major, so
+  // tier t's pairs are a contiguous range of it.  One launch (the widest front the batch
+  // needs) in input order, with a shared queue, or when tracing.
+  const bool split = k16 && !tr && !b->queue && !(b->flags & (AGATHA_ORDER_INPUT | AGATHA_SINGLE_TIER));
+  int tiers_launched = 0, slots = 0;
+  memset(ctx->stats.tier_pairs, 0, sizeof(ctx->stats.tier_pairs));
+  if (split) {
+    CUDA_TRY(cudaEventRecord(ctx->tev[0], st));
+    uint32_t start = 0;
+    for (int t = 0; t < 3 && !rc; ++t) {
+      if (tier_n[t] == 0) continue;
+      AlignArgs At = A;
+      At.order = d_order + start;
+      At.n_pairs = (uint32_t)tier_n[t];
+      At.queue = t == 0 ? d_sc + 2 : d_sc + 7 + t;
+      start += (uint32_t)tier_n[t];
+      cudaStream_t ts = st;
+      if (t > 0) {
+        ts = ctx->tier_stream[t - 1];
+        CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tev[0], 0));
+      }
+      int g = 0;
+      if (t == 0) rc = maxoff16_t0 <= 8 ? launch_align16<16, false, 8>(ctx, At, ts, &g)
+                                        : launch_align16<16, false, 16>(ctx, At, ts, &g);
+      else if (t == 1) rc = launch_align16<8, false, 8>(ctx, At, ts, &g);
+      else rc = launch_align16<4, false, 3>(ctx, At, ts, &g);
+      if (t > 0) CUDA_TRY(cudaEventRecord(ctx->tev[t], ts));
+      grid += g;
+      ++tiers_launched;
+      ctx->stats.tier_pairs[t] = tier_n[t];
+      if (!slots) slots = 32 >> t;
+    }
+    for (int t = 1; t < 3; ++t)
+      if (tier_n[t]) CUDA_TRY(cudaStreamWaitEvent(st, ctx->tev[t], 0));
+  } else if (k16) {
     // (NREG = 16) eight capped registers suffice when every pair's low padding
     // off = (-D) mod 16 is at most 8 (prep_kernel's max); else all sixteen
-    if (K == 16) rc = tr ? launch_align16<8, true, 8>(ctx, A, st, &grid) : launch_align16<8, false, 8>(ctx, A, st, &grid);
+    const int t = tier_of(maxD);
+    if (t == 2) rc = tr ? launch_align16<4, true, 3>(ctx, A, st, &grid) : launch_align16<4, false, 3>(ctx, A, st, &grid);
+    else if (t == 1) rc = tr ? launch_align16<8, true, 8>(ctx, A, st, &grid) : launch_align16<8, false, 8>(ctx, A, st, &grid);
     else if (tr) rc = launch_align16<16, true, 16>(ctx, A, st, &grid);
     else if (maxoff16 <= 8) rc = launch_align16<16, false, 8>(ctx, A, st, &grid);
     else rc = launch_align16<16, false, 16>(ctx, A, st, &grid);
+    tiers_launched = 1;
+    ctx->stats.tier_pairs[t] = (int)P;
+    slots = 32 >> t;
   } else {
     if (K == 16) rc = tr ? launch_align<16, true>(ctx, A, st, &grid) : launch_align<16, false>(ctx, A, st, &grid);
     else if (maxD <= kMaxSlots) rc = tr ? launch_align<32, true>(ctx, A, st, &grid) : launch_align<32, false>(ctx, A, st, &grid);
     else if (maxD <= 2 * kMaxSlots)  // NEXT #3: wide bands, two or four warps per pair
       rc = tr ? launch_align_wide<2, true>(ctx, A, st, &grid) : launch_align_wide<2, false>(ctx, A, st, &grid);
     else rc = tr ? launch_align_wide<4, true>(ctx, A, st, &grid) : launch_align_wide<4, false>(ctx, A, st, &grid);
+    tiers_launched = 1;
+    slots = K;
   }
   ctx->stats.packed16 = k16 ? 1 : 0;
   if (rc) {
     if (!dev_in) cudaStreamSynchronize(ctx->copy_stream);
     return rc;
   }
-  ++launches;
+  launches += tiers_launched;
   CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
   if (!dev_out)
     CUDA_TRY(cudaMemcpyAsync(out, d_out, sizeof(agatha_result_t) * P, cudaMemcpyDeviceToHost, st));
@@ -1732,7 +1819,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   cudaEventElapsedTime(&ctx->stats.prep_ms, ctx->ev[1], ctx->ev[2]);
   cudaEventElapsedTime(&ctx->stats.align_ms, ctx->ev[2], ctx->ev[3]);
   cudaEventElapsedTime(&ctx->stats.d2h_ms, ctx->ev[3], ctx->ev[4]);
-  ctx->stats.slots_per_lane = K;
+  ctx->stats.slots_per_lane = slots;
   ctx->stats.warps_per_pair = k16 || maxD <= kMaxSlots ? 1 : (maxD <= 2 * kMaxSlots ? 2 : 4);
   ctx->stats.grid_blocks = grid;
   ctx->stats.kernel_launches = launches;
@@ -1776,7 +1863,9 @@ int agatha_ctx_create(agatha_ctx_t** out, int device) {
   ctx->num_sms = prop.multiProcessorCount;
   for (int i = 0; i < 6; ++i) cudaEventCreate(&ctx->ev[i]);
   for (int i = 0; i < 2; ++i) cudaEventCreate(&ctx->cev[i]);
+  for (int i = 0; i < 3; ++i) cudaEventCreateWithFlags(&ctx->tev[i], cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2; ++i) cudaStreamCreateWithFlags(&ctx->tier_stream[i], cudaStreamNonBlocking);
   if (cudaMallocHost(&ctx->h_scalars, 64) != cudaSuccess ||
       cudaMallocHost(&ctx->h_ones, 4 * kMaxChunks) != cudaSuccess ||
       cudaMallocHost(&ctx->h_chunk_first, 8 * (kMaxChunks + 1)) != cudaSuccess) {
@@ -1799,7 +1888,10 @@ void agatha_ctx_destroy(agatha_ctx_t* ctx) {
     if (b->p) cudaFree(b->p);
   for (int i = 0; i < 6; ++i) cudaEventDestroy(ctx->ev[i]);
   for (int i = 0; i < 2; ++i) cudaEventDestroy(ctx->cev[i]);
+  for (int i = 0; i < 3; ++i) cudaEventDestroy(ctx->tev[i]);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (int i = 0; i < 2; ++i)
+    if (ctx->tier_stream[i]) cudaStreamDestroy(ctx->tier_stream[i]);
   if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
   if (ctx->h_ones) cudaFreeHost(ctx->h_ones);
   if (ctx->h_chunk_first) cudaFreeHost(ctx->h_chunk_first);
@@ -1881,6 +1973,7 @@ int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* b, const agatha_params_
   pa.nominal = nominal; pa.iota = (uint32_t*)ctx->iota.p;
   pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1; pa.max_off16 = d_sc + 3;
   pa.chunk_first = nullptr; pa.nchunks = 1; pa.chunk_of = nullptr; pa.key64 = nullptr;
+  pa.tier_shift = 32; pa.tier_count = nullptr; pa.max_off16_t0 = nullptr;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
   CUDA_TRY(cudaGetLastError());

@@ -62,7 +62,9 @@ def test_random_short_pairs(gpu_lib, ctx, kflags, band):
 # eight-cap kernel for off <= 8 and the sixteen-cap one above): DESIGN.md §6.1 "Layout".
 @pytest.mark.parametrize("bl,br", [(256, 255), (255, 255), (250, 255), (249, 254), (100, 3),
                                    (504, 504), (503, 504), (500, 500), (300, 292), (511, 511),
-                                   (511, 500), (0, 600), (600, 0), (264, 264)])
+                                   (511, 500), (0, 600), (600, 0), (264, 264),
+                                   # NREG = 4 (the narrow slot tier, D <= 256): off = 0..3
+                                   (127, 128), (127, 127), (126, 127), (126, 126), (64, 64)])
 def test_band_layouts_long_pairs(gpu_lib, ctx, bl, br):
     rng = np.random.default_rng(7000 + bl * 1000 + br)
     lst = []
@@ -159,6 +161,48 @@ def test_config_subsets(gpu_lib, ctx, kflags, name, k0, k1):
     cfg = synth.CONFIGS[name]
     pairs = synth.generate(cfg, k0, k1)
     compare(gpu_lib, ctx, pairs, vars(cfg.scoring), flags=kflags)
+
+
+def _tier(m, n, bl, br):
+    """Slot tier of a pair (DESIGN.md §6.1 "Slot tiers"): 0, 1, 2 for a 32-lane front of
+    32, 16, 8 slots per lane, the narrowest that holds the pair's D clipped diagonals."""
+    D = min(bl, n) + min(br, m) + 1
+    return 0 if D > 512 else (1 if D > 256 else 2)
+
+
+def test_slot_tiers_mixed_batch(gpu_lib, ctx):
+    """A batch whose pairs need all three slot tiers (w = 500; short pairs clip the band):
+    every tier launch is bit-exact, the per-tier counts match the pairs' D, and one launch
+    at the widest front (SINGLE_TIER) or input order gives the same bytes."""
+    rng = np.random.default_rng(4242)
+    lst = []
+    for k in range(240):
+        L = int([rng.integers(20, 120), rng.integers(130, 250), rng.integers(300, 1500)][k % 3])
+        a = "".join("ACGT"[x] for x in rng.integers(0, 4, L))
+        q = "".join(c if rng.random() > 0.04 else "ACGT"[int(rng.integers(0, 4))] for c in a)
+        if k % 5 == 0:  # chimeric tail: Z-drop fires
+            cut = int(rng.integers(1, len(q)))
+            q = q[:cut] + "".join("ACGT"[x] for x in rng.integers(0, 4, len(q) - cut))
+        lst.append((a, q[: int(rng.integers(max(1, len(q) // 2), len(q) + 1))]))
+    pairs = synth.from_list(lst)
+    params = dict(SCORING, band_left=500, band_right=500, zdrop=60)
+    got = compare(gpu_lib, ctx, pairs, params)
+    want = [0, 0, 0]
+    for R, Q in lst:
+        want[_tier(len(R), len(Q), 500, 500)] += 1
+    assert min(want) > 0
+    st = ctx.stats()
+    assert st["packed16"] == 1 and st["tier_pairs"] == want, (st, want)
+    assert st["kernel_launches"] == 1 + 3  # prep + one align launch per tier
+    one = gpu_lib.align_pairs(ctx, pairs, params, flags=gpu_lib.SINGLE_TIER)
+    assert ctx.stats()["tier_pairs"] == [len(lst), 0, 0]
+    assert one.tobytes() == got.tobytes()
+    inp = gpu_lib.align_pairs(ctx, pairs, params, flags=gpu_lib.ORDER_INPUT)
+    assert inp.tobytes() == got.tobytes()
+    # a batch that is all narrow runs the NREG = 4 front alone
+    short = pairs.subset([k for k in range(len(lst)) if k % 3 == 0])
+    compare(gpu_lib, ctx, short, params)
+    assert ctx.stats()["tier_pairs"] == [0, 0, short.n_pairs] and ctx.stats()["slots_per_lane"] == 8
 
 
 def test_kernel_selection(gpu_lib, ctx):
