@@ -769,6 +769,13 @@ __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A)
 #ifndef AGATHA_FMA_ADD
 #define AGATHA_FMA_ADD 1
 #endif
+// A/B switches (DESIGN.md §6.5 "Tried and reverted"); the defaults are the measured best
+#ifndef AGATHA_RREUSE
+#define AGATHA_RREUSE 0  // 1: carry the PAR = 1 R shift into the next PAR = 0 step (-1.6%)
+#endif
+#ifndef AGATHA_VOTE
+#define AGATHA_VOTE 1    // 0: plain uniform branch instead of the vote in process16 (-0.2%)
+#endif
 constexpr int kW16 = -29250;       // "-infinity" (walls, E/F of boundary cells)
 constexpr int kCapNeg16 = -21250;  // padding cap
 constexpr int kEmpty16 = -17250;   // lane max at or below: no valid cell on the anti-diagonal
@@ -872,7 +879,13 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
   const int Hs = rH + Bc - s.alpha * c;
   const bool upd = nonempty && Hs > s.G_H;
   const bool chk = nonempty && Hs < s.zthr && ((STEADY && !TRACE) || c < s.mn);
+  // upd and chk are warp-uniform (rH is a warp reduction, the rest is per-pair state):
+  // a plain uniform branch, no vote
+#if AGATHA_VOTE
   if (!__any_sync(kFull, upd || chk || (TRACE && nonempty))) return false;
+#else
+  if (!(upd || chk || (TRACE && nonempty))) return false;
+#endif
   if (TRACE || chk) {
     uint32_t r[NREG / 2];
 #pragma unroll
@@ -1098,10 +1111,11 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   int iters = 0;
 
   // substitution pairs (cells t, t+NC/2) of one step, from the nibble windows
-  auto scores = [&](uint32_t (&S2)[NREG / 2], const uint32_t (&Wr)[3], const uint32_t (&qg)[2], int shiftR) {
+  // rs: the R window shifted to the step's first cell (rshift)
+  auto scores = [&](uint32_t (&S2)[NREG / 2], const uint32_t (&rs)[2], const uint32_t (&qg)[2]) {
     if (NREG == 16) {
-      const uint32_t x0 = combine(__funnelshift_rc(Wr[0], Wr[1], shiftR), qg[0]);
-      const uint32_t x1 = combine(__funnelshift_rc(Wr[1], Wr[2], shiftR), qg[1]);
+      const uint32_t x0 = combine(rs[0], qg[0]);
+      const uint32_t x1 = combine(rs[1], qg[1]);
       const uint32_t a0 = prmt(T0, T1, x0), a1 = prmt(T0, T1, shr16_fma(x0, k65536));
       const uint32_t b0 = prmt(T0, T1, x1), b1 = prmt(T0, T1, shr16_fma(x1, k65536));
 #pragma unroll
@@ -1110,7 +1124,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         S2[k] = prmt(k < 4 ? a0 : a1, k < 4 ? b0 : b1, b | ((b | 8) << 4) | ((4 + b) << 8) | (((4 + b) | 8) << 12));
       }
     } else if (NREG == 8) {  // cells 0..7 in one word, pairs (t, t+4)
-      const uint32_t x0 = combine(__funnelshift_rc(Wr[0], Wr[1], shiftR), qg[0]);
+      const uint32_t x0 = combine(rs[0], qg[0]);
       const uint32_t a0 = prmt(T0, T1, x0), a1 = prmt(T0, T1, shr16_fma(x0, k65536));
 #pragma unroll
       for (int k = 0; k < NREG / 2; ++k) {
@@ -1118,7 +1132,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         S2[k] = prmt(a0, a1, b | ((b | 8) << 4) | ((4 + b) << 8) | (((4 + b) | 8) << 12));
       }
     } else {  // NREG == 4 (narrow tier): cells 0..3 from the low half-word, pairs (t, t+2)
-      const uint32_t x0 = combine(__funnelshift_rc(Wr[0], Wr[1], shiftR), qg[0]);
+      const uint32_t x0 = combine(rs[0], qg[0]);
       const uint32_t a0 = prmt(T0, T1, x0);
 #pragma unroll
       for (int k = 0; k < NREG / 2; ++k) {
@@ -1135,15 +1149,28 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     return (v & ((1u << (NC / 2)) - 1u)) | ((v >> (NC / 2)) << 16);
   };
 
+  auto rshift = [&](uint32_t (&rs)[2], int sh) {
+    rs[0] = __funnelshift_rc(Wr0, Wr1, sh);
+    if (NREG == 16) rs[1] = __funnelshift_rc(Wr1, Wr2, sh);
+  };
+  // The R window shifted for the PAR = 1 step (4*oR + 4) is the next iteration's PAR = 0
+  // shift (oR advances by one), also across a refill: the clamped shift by 32 returns
+  // the second word, which the refill makes the first.
+  uint32_t rsc[2] = {0u, 0u};
+  rshift(rsc, 4 * oR);
   auto iteration = [&](auto masked_tag) {
     constexpr bool MASKED = decltype(masked_tag)::value;
-    uint32_t qg[2], S2[NREG / 2], V2 = 0u;
-    const uint32_t Wq[3] = {Wq0, Wq1, Wq2}, Wr[3] = {Wr0, Wr1, Wr2};
-    qg[0] = __funnelshift_rc(Wq[0], Wq[1], 4 * oQ);
-    qg[1] = __funnelshift_rc(Wq[1], Wq[2], 4 * oQ);
+    uint32_t qg[2], S2[NREG / 2], V2 = 0u, rs[2];
+    qg[0] = __funnelshift_rc(Wq0, Wq1, 4 * oQ);
+    qg[1] = __funnelshift_rc(Wq1, Wq2, 4 * oQ);
     // ---- step PAR = 0, anti-diagonal cb ----
     {
-      scores(S2, Wr, qg, 4 * oR);
+#if AGATHA_RREUSE
+      scores(S2, rsc, qg);
+#else
+      rshift(rs, 4 * oR);
+      scores(S2, rs, qg);
+#endif
       int tlo = 0, thi = NC;
       if (MASKED) {
         const int ib = u + lane * NC, jb = u - dls - lane * NC;
@@ -1161,7 +1188,12 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     }
     // ---- step PAR = 1, anti-diagonal cb + 1 ----
     {
-      scores(S2, Wr, qg, 4 * oR + 4);
+      rshift(rs, 4 * oR + 4);
+      scores(S2, rs, qg);
+#if AGATHA_RREUSE
+      rsc[0] = rs[0];
+      rsc[1] = rs[1];
+#endif
       int tlo = 0, thi = NC;
       if (MASKED) {
         const int ib = u + 1 + lane * NC, jb = u - dls - lane * NC;
@@ -1531,6 +1563,18 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
   return AGATHA_OK;
 }
 
+// NREG = 16: the capped registers must cover every pair's low padding off = (-D) mod 16
+#ifndef AGATHA_NCAP7
+#define AGATHA_NCAP7 0  // 1: seven capped registers when every off <= 7 (-0.1%)
+#endif
+int launch_align16_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int maxoff) {
+#if AGATHA_NCAP7
+  if (maxoff <= 7) return launch_align16<16, false, 7>(ctx, A, st, grid_out);
+#endif
+  if (maxoff <= 8) return launch_align16<16, false, 8>(ctx, A, st, grid_out);
+  return launch_align16<16, false, 16>(ctx, A, st, grid_out);
+}
+
 template <int W, bool TRACE>
 int launch_align_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
   static int occ = -1;
@@ -1767,8 +1811,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
         CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tev[0], 0));
       }
       int g = 0;
-      if (t == 0) rc = maxoff16_t0 <= 8 ? launch_align16<16, false, 8>(ctx, At, ts, &g)
-                                        : launch_align16<16, false, 16>(ctx, At, ts, &g);
+      if (t == 0) rc = launch_align16_wide(ctx, At, ts, &g, maxoff16_t0);
       else if (t == 1) rc = launch_align16<8, false, 8>(ctx, At, ts, &g);
       else rc = launch_align16<4, false, 3>(ctx, At, ts, &g);
       if (t > 0) CUDA_TRY(cudaEventRecord(ctx->tev[t], ts));
@@ -1786,8 +1829,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     if (t == 2) rc = tr ? launch_align16<4, true, 3>(ctx, A, st, &grid) : launch_align16<4, false, 3>(ctx, A, st, &grid);
     else if (t == 1) rc = tr ? launch_align16<8, true, 8>(ctx, A, st, &grid) : launch_align16<8, false, 8>(ctx, A, st, &grid);
     else if (tr) rc = launch_align16<16, true, 16>(ctx, A, st, &grid);
-    else if (maxoff16 <= 8) rc = launch_align16<16, false, 8>(ctx, A, st, &grid);
-    else rc = launch_align16<16, false, 16>(ctx, A, st, &grid);
+    else rc = launch_align16_wide(ctx, A, st, &grid, maxoff16);
     tiers_launched = 1;
     ctx->stats.tier_pairs[t] = (int)P;
     slots = 32 >> t;
