@@ -1304,10 +1304,22 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   }
 }
 
+// Warps per block and blocks per SM of each front (A/B: AGATHA_WPB16 / AGATHA_MINB16)
+#ifndef AGATHA_WPB16
+#define AGATHA_WPB16 4
+#endif
+#ifndef AGATHA_MINB16
+#define AGATHA_MINB16 3
+#endif
+template <int NREG> struct Front16 {
+  static constexpr int wpb = NREG >= 16 ? AGATHA_WPB16 : 4;
+  static constexpr int minb = NREG >= 16 ? AGATHA_MINB16 : (NREG >= 8 ? 4 : 5);
+};
+
 template <int NREG, bool TRACE, int NCAP>
-__global__ void __launch_bounds__(128, NREG >= 16 ? 3 : (NREG >= 8 ? 4 : 5)) align16_kernel(AlignArgs A) {
-  __shared__ uint32_t snap_all[4][NREG / 2 * 32];
-  __shared__ uint32_t pref_all[4][64];
+__global__ void __launch_bounds__(32 * Front16<NREG>::wpb, Front16<NREG>::minb) align16_kernel(AlignArgs A) {
+  __shared__ uint32_t snap_all[Front16<NREG>::wpb][NREG / 2 * 32];
+  __shared__ uint32_t pref_all[Front16<NREG>::wpb][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (;;) {
     int q = 0;
@@ -1547,18 +1559,20 @@ template <int NREG, bool TRACE, int NCAP>
 int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
   static int occ = -1;
   if (occ < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align16_kernel<NREG, TRACE, NCAP>, 128, 0) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align16_kernel<NREG, TRACE, NCAP>,
+                                                      32 * Front16<NREG>::wpb, 0) != cudaSuccess) {
       cudaGetLastError();
       occ = 1;
     }
     if (occ < 1) occ = 1;
   }
   const long long want = (long long)ctx->num_sms * occ;
-  const long long need = ((long long)A.n_pairs + 3) / 4;
+  constexpr int wpb = Front16<NREG>::wpb;
+  const long long need = ((long long)A.n_pairs + wpb - 1) / wpb;
   int grid = (int)(want < need ? want : need);
   if (grid < 1) grid = 1;
   *grid_out = grid;
-  align16_kernel<NREG, TRACE, NCAP><<<grid, 128, 0, st>>>(A);
+  align16_kernel<NREG, TRACE, NCAP><<<grid, 32 * wpb, 0, st>>>(A);
   CUDA_TRY(cudaGetLastError());
   return AGATHA_OK;
 }

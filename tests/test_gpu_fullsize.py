@@ -23,7 +23,7 @@ def ctx(gpu_lib):
     c.close()
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5", "LS10"])
 def test_full_size_sampled_parity(gpu_lib, ctx, name):
     import torch
 
@@ -54,8 +54,15 @@ def test_full_size_sampled_parity(gpu_lib, ctx, name):
     assert np.all(got["cells"][:2000] <= nominal)
     assert np.all(got["cells"][:2000][term[:2000] < 0] == nominal[term[:2000] < 0])
 
-    # sampled exact parity
+    # slot tiers: each pair at the narrowest front holding its clipped band
+    D = np.minimum(params["band_left"], n) + np.minimum(params["band_right"], m) + 1
+    tier = np.where(D > 512, 0, np.where(D > 256, 1, 2))
+    assert ctx.stats()["tier_pairs"] == [int((tier == t).sum()) for t in range(3)]
+
+    # sampled exact parity: evenly spaced pairs plus a few of every tier present
     idx = np.linspace(0, pairs.n_pairs - 1, SAMPLE).astype(np.int64)
+    for t in range(3):
+        idx = np.concatenate([idx, np.nonzero(tier == t)[0][:6]])
     rc, exp, _ = oracle.align_batch(pairs.subset(idx), params)
     assert rc == 0
     bad = np.nonzero(got[idx] != exp)[0]
