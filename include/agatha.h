@@ -123,6 +123,9 @@ typedef struct {
   int32_t warps_per_pair; /* 1; 2 or 4 in the wide-band tier (D > 1024, 32-bit)          */
   int32_t tier_pairs[3]; /* 16-bit kernel: pairs run at 32 / 16 / 8 slots per lane (the
                             slot tiers for D > 512 / 257..512 / <= 256 diagonals)         */
+  int32_t input_chunks;  /* host inputs: chunks streamed under the kernel (1 for device)  */
+  int32_t lpt_from_chunk; /* chunks from this one on are dispatched as one longest-first
+                             group (they arrive before the queue reaches them)           */
 } agatha_stats_t;
 
 /* Create a context on CUDA device `cuda_device`.  Fails with AGATHA_ECUDA when the

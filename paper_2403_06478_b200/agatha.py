@@ -56,7 +56,8 @@ class Stats(ctypes.Structure):
                 ("slots_per_lane", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
                 ("kernel_launches", ctypes.c_int32), ("library_launches", ctypes.c_int32),
                 ("packed16", ctypes.c_int32), ("warps_per_pair", ctypes.c_int32),
-                ("tier_pairs", ctypes.c_int32 * 3)]
+                ("tier_pairs", ctypes.c_int32 * 3), ("input_chunks", ctypes.c_int32),
+                ("lpt_from_chunk", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: (list(v) if k == "tier_pairs" else v)

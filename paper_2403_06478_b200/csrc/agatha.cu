@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -1361,6 +1362,8 @@ struct PrepArgs {
   uint64_t* key64;              // out: dispatch key (tier << tier_shift) | (chunk << 32) | ~nominal,
                                 // ascending: tier-major, chunk-major, longest first
   int tier_shift;               // 32 + chunk-id bits
+  int lpt_from;                 // chunks >= lpt_from share one key group (one longest-first
+                                // range): the queue reaches them after they have arrived
   int* tier_count;              // [3] pairs per slot tier (tier_of)
   int* max_off16_t0;            // max (-D) mod 16 over the pairs of tier 0
 };
@@ -1414,7 +1417,8 @@ __global__ void prep_kernel(PrepArgs P) {
         }
         P.chunk_of[p] = (uint8_t)lo;
         const uint64_t tier = flag ? 0 : (uint64_t)tier_of(D);
-        P.key64[p] = (tier << P.tier_shift) | ((uint64_t)lo << 32) | (uint64_t)(0xffffffffu - nom);
+        const uint64_t grp = (uint64_t)(lo < P.lpt_from ? lo : P.lpt_from);
+        P.key64[p] = (tier << P.tier_shift) | (grp << 32) | (uint64_t)(0xffffffffu - nom);
       }
       P.bad[p] = (uint8_t)(flag != 0);
       if (flag) {
@@ -1687,6 +1691,26 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     }
   }
   ctx->h_chunk_first[nchunks] = P;
+  // Streamed inputs: the order is chunk-major so that no warp waits on a
+  // chunk still in flight, but then a long pair of a late chunk starts late and ends
+  // after everything else (the tail).  The queue reaches chunk c after about c/nchunks
+  // of the kernel time, while every chunk has arrived after the copy time; from the
+  // first chunk the queue reaches after the copies end, all later chunks form one
+  // longest-first group.  Estimates (conservative: a fast kernel, a slow link):
+  // kernel = sum min(m,n)*D / 4 TCUPS, copy = bytes / 20 GB/s, margin 1.25.
+  int lpt_from = nchunks;
+  if (!dev_in && nchunks > 2) {
+    double cells = 0.0;
+    for (uint64_t k = 0; k < P; ++k) {
+      const int64_t m = (int64_t)(b->ref_off[k + 1] - b->ref_off[k]), n = (int64_t)(b->qry_off[k + 1] - b->qry_off[k]);
+      const int64_t bl = (p->band_left < 0 || p->band_left > n) ? n : p->band_left;
+      const int64_t br = (p->band_right < 0 || p->band_right > m) ? m : p->band_right;
+      cells += (double)(m < n ? m : n) * (double)(bl + br + 1);
+    }
+    const double t_kernel = cells / 4e12, t_copy = (double)(tot_r + tot_q) / 20e9;
+    const double f = t_kernel > 0 ? 1.25 * t_copy / t_kernel : 1.0;
+    if (f < 1.0) lpt_from = std::max(1, (int)std::ceil(f * nchunks));
+  }
   CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
 
   // device scratch
@@ -1733,6 +1757,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   int chunk_bits = 0;
   while ((1 << chunk_bits) < nchunks) ++chunk_bits;
   pa.tier_shift = 32 + chunk_bits; pa.tier_count = d_sc + 4; pa.max_off16_t0 = d_sc + 7;
+  pa.lpt_from = lpt_from;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
   CUDA_TRY(cudaGetLastError());
@@ -1878,6 +1903,8 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   ctx->stats.slots_per_lane = slots;
   ctx->stats.warps_per_pair = k16 || maxD <= kMaxSlots ? 1 : (maxD <= 2 * kMaxSlots ? 2 : 4);
   ctx->stats.grid_blocks = grid;
+  ctx->stats.input_chunks = nchunks;
+  ctx->stats.lpt_from_chunk = lpt_from;
   ctx->stats.kernel_launches = launches;
   ctx->stats.library_launches = lib_launches;
   return AGATHA_OK;
@@ -2029,7 +2056,7 @@ int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* b, const agatha_params_
   pa.nominal = nominal; pa.iota = (uint32_t*)ctx->iota.p;
   pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1; pa.max_off16 = d_sc + 3;
   pa.chunk_first = nullptr; pa.nchunks = 1; pa.chunk_of = nullptr; pa.key64 = nullptr;
-  pa.tier_shift = 32; pa.tier_count = nullptr; pa.max_off16_t0 = nullptr;
+  pa.tier_shift = 32; pa.tier_count = nullptr; pa.max_off16_t0 = nullptr; pa.lpt_from = 1;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
   CUDA_TRY(cudaGetLastError());

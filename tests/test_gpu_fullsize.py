@@ -69,3 +69,9 @@ def test_full_size_sampled_parity(gpu_lib, ctx, name):
     assert len(bad) == 0, f"{name}: pair {idx[bad[0]]} gpu={got[idx[bad[0]]]} oracle={exp[bad[0]]}"
     if name == "C3":
         assert (term >= 0).mean() > 0.2  # the Z-drop-heavy configuration really terminates
+        # host inputs stream in chunks under the kernel, the late chunks
+        # dispatched as one longest-first group: the same bytes as the device-input run
+        host = gpu_lib.align_pairs(ctx, pairs, params)
+        st = ctx.stats()
+        assert st["input_chunks"] > 2 and 1 <= st["lpt_from_chunk"] < st["input_chunks"], st
+        assert host.tobytes() == got.tobytes()
