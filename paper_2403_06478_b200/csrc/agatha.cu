@@ -774,6 +774,17 @@ __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A)
 #ifndef AGATHA_RREUSE
 #define AGATHA_RREUSE 0  // 1: carry the PAR = 1 R shift into the next PAR = 0 step (-1.6%)
 #endif
+#ifndef AGATHA_LMSHL
+#define AGATHA_LMSHL 1  // lane max of the two halves via lm << 16 (IMAD) instead of hi16_fma
+#endif
+#if AGATHA_LMSHL
+#define LANEMAX16(x) ((x) >> 16)
+#else
+#define LANEMAX16(x) (x)
+#endif
+#ifndef AGATHA_S2EARLY
+#define AGATHA_S2EARLY 0  // 1: both steps' substitution scores at the top of the iteration
+#endif
 #ifndef AGATHA_VOTE
 #define AGATHA_VOTE 1    // 0: plain uniform branch instead of the vote in process16 (-0.2%)
 #endif
@@ -792,12 +803,19 @@ __device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vma
 // x >> 16 (logical / arithmetic) as the high word of x * 65536 on the FMA pipe: the
 // kernel is ALU-pipe bound and the FMA pipe is ~85% idle.  k65536 is passed at run time
 // so that ptxas cannot strength-reduce the multiply back into an ALU shift.
+#ifndef AGATHA_SHR_WIDE
+#define AGATHA_SHR_WIDE 0  // 1: x >> 16 as the high word of a 64-bit IMAD.WIDE
+#endif
 __device__ __forceinline__ uint32_t shr16_fma(uint32_t x, uint32_t k65536) {
   uint32_t d;
+#if AGATHA_SHR_WIDE
+  asm("{\n\t.reg .u64 w;\n\tmul.wide.u32 w, %1, %2;\n\tmov.b64 {_, %0}, w;\n\t}" : "=r"(d) : "r"(x), "r"(k65536));
+#else
   asm("mad.hi.u32 %0, %1, %2, 0;" : "=r"(d) : "r"(x), "r"(k65536));
+#endif
   return d;
 }
-__device__ __forceinline__ int hi16_fma(uint32_t x, uint32_t k65536) {
+[[maybe_unused]] __device__ __forceinline__ int hi16_fma(uint32_t x, uint32_t k65536) {
   int d;
   asm("mad.hi.s32 %0, %1, %2, 0;" : "=r"(d) : "r"((int)x), "r"((int)k65536));
   return d;
@@ -989,7 +1007,14 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
   // max of the two halves as an int32: hi16_fma gives (sign(hi) = -1 : hi), and every
   // H half is negative (<= kTop16), so the pair max is (-1 : max(lo, hi)), which read as
   // an int32 is exactly max(lo, hi)
+#if AGATHA_LMSHL
+  // (lm << 16 as a full-rate IMAD): the high half becomes max(hi, lo) and the low half
+  // max(lo, 0) = 0, so the lane value is max(lo, hi) * 65536 and the warp max is
+  // recovered by one uniform shift after the REDUX (LANEMAX16)
+  return (int)vmax2(lm, lm * k65536);
+#else
   return (int)vmax2(lm, (uint32_t)hi16_fma(lm, k65536));
+#endif
 }
 
 template <int NREG, bool TRACE, int NCAP>
@@ -1164,6 +1189,13 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     uint32_t qg[2], S2[NREG / 2], V2 = 0u, rs[2];
     qg[0] = __funnelshift_rc(Wq0, Wq1, 4 * oQ);
     qg[1] = __funnelshift_rc(Wq1, Wq2, 4 * oQ);
+#if AGATHA_S2EARLY
+    // both steps' scores up front: the PAR = 1 lookups (with their long-latency IMAD.HI)
+    // then issue under the PAR = 0 cells instead of stalling in front of PAR = 1
+    uint32_t S2b[NREG / 2];
+    rshift(rs, 4 * oR + 4);
+    scores(S2b, rs, qg);
+#endif
     // ---- step PAR = 0, anti-diagonal cb ----
     {
 #if AGATHA_RREUSE
@@ -1180,7 +1212,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         V2 = valid_bits(tlo, thi);
       }
       const int lmax = step16<NREG, NCAP, 0, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
-      const int rH = __reduce_max_sync(kFull, lmax);
+      const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
       B_prev = s.B;
@@ -1189,8 +1221,13 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     }
     // ---- step PAR = 1, anti-diagonal cb + 1 ----
     {
+#if AGATHA_S2EARLY
+#pragma unroll
+      for (int k = 0; k < NREG / 2; ++k) S2[k] = S2b[k];
+#else
       rshift(rs, 4 * oR + 4);
       scores(S2, rs, qg);
+#endif
 #if AGATHA_RREUSE
       rsc[0] = rs[0];
       rsc[1] = rs[1];
@@ -1203,7 +1240,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         V2 = valid_bits(tlo, thi);
       }
       const int lmax = step16<NREG, NCAP, 1, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
-      const int rH = __reduce_max_sync(kFull, lmax);
+      const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
       B_prev = s.B;
