@@ -49,8 +49,9 @@ OPS_PER_CELL_32 = 4.5
 SM_COUNT = 148
 LANES_PER_CLK_PER_SM = 64
 # dram__bytes_read.sum + dram__bytes_write.sum per align launch on the full C2 batch, from
-# one `ncu --set full` capture (profiles/r01_ncu_*_summary.csv); updated per profile.
-TRAFFIC = {"align_kernel<32>": 1.603e9 + 0.0748e9, "align16_kernel<16>": 3.324e9 + 1.506e9}
+# one ncu capture (profiles/r01c_ncu_align16_dram_c2.csv, r01_ncu_align_kernel_summary.csv);
+# updated per profile.
+TRAFFIC = {"align_kernel<32>": 1.603e9 + 0.0748e9, "align16_kernel<16>": 3.328e9 + 1.545e9}
 
 
 def parse():
