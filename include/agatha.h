@@ -129,7 +129,9 @@ typedef struct {
 } agatha_stats_t;
 
 /* Create a context on CUDA device `cuda_device`.  Fails with AGATHA_ECUDA when the
- * device is not an sm_100 part. */
+ * device is not an sm_100 part.  Host inputs stream to the device in chunks of ~48 MB of
+ * ASCII; the environment variable AGATHA_CHUNK_BYTES (>= 256), read here, overrides the
+ * chunk size (tests use it to exercise many chunks on small batches). */
 int agatha_ctx_create(agatha_ctx_t** ctx, int cuda_device);
 void agatha_ctx_destroy(agatha_ctx_t* ctx);
 

@@ -1499,6 +1499,8 @@ struct agatha_ctx {
   int* h_ones = nullptr;                              // pinned 1s (chunk-arrival flags)
   uint64_t* h_chunk_first = nullptr;                  // pinned chunk boundaries
   cudaStream_t copy_stream = nullptr;                 // H2D of input chunks
+  uint64_t chunk_bytes = kChunkBytes;                 // target ASCII bytes per chunk
+                                                      // (env AGATHA_CHUNK_BYTES, for tests)
   cudaEvent_t ev[6];
   cudaEvent_t cev[2];
   cudaStream_t tier_stream[2] = {nullptr, nullptr};  // slot tiers 1 and 2
@@ -1715,7 +1717,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     d_qry = (const uint8_t*)ctx->qry_ascii.p;
     d_roff = (const uint64_t*)ctx->ref_off.p;
     d_qoff = (const uint64_t*)ctx->qry_off.p;
-    uint64_t target = kChunkBytes;
+    uint64_t target = ctx->chunk_bytes;
     const uint64_t total = tot_r + tot_q;
     if (total / target + 2 > (uint64_t)kMaxChunks) target = total / (kMaxChunks - 2) + 1;
     uint64_t acc = 0;
@@ -1981,6 +1983,10 @@ int agatha_ctx_create(agatha_ctx_t** out, int device) {
   agatha_ctx* ctx = new agatha_ctx();
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
+  if (const char* e = getenv("AGATHA_CHUNK_BYTES")) {
+    const unsigned long long v = strtoull(e, nullptr, 10);
+    if (v >= 256) ctx->chunk_bytes = v;
+  }
   for (int i = 0; i < 6; ++i) cudaEventCreate(&ctx->ev[i]);
   for (int i = 0; i < 2; ++i) cudaEventCreate(&ctx->cev[i]);
   for (int i = 0; i < 3; ++i) cudaEventCreateWithFlags(&ctx->tev[i], cudaEventDisableTiming);

@@ -205,6 +205,33 @@ def test_slot_tiers_mixed_batch(gpu_lib, ctx):
     assert ctx.stats()["tier_pairs"] == [0, 0, short.n_pairs] and ctx.stats()["slots_per_lane"] == 8
 
 
+def test_streamed_host_chunks(gpu_lib, monkeypatch):
+    """Host inputs stream in many small chunks (AGATHA_CHUNK_BYTES shrinks them) under the
+    running kernel, warps waiting on per-chunk arrival flags, the late chunks dispatched as
+    one longest-first group: identical bytes to the device-input run."""
+    import torch
+    monkeypatch.setenv("AGATHA_CHUNK_BYTES", "262144")
+    c = gpu_lib.Context(0)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    for name, k1, grouped in (("C2", 200, True), ("C1", 1000, False)):
+        cfg = synth.CONFIGS[name]
+        pairs = synth.generate(cfg, 0, k1)
+        params = vars(cfg.scoring)
+        host = gpu_lib.align_pairs(c, pairs, params)
+        st = c.stats()
+        assert st["input_chunks"] > 4, st
+        # w = 500 is compute-bound (late chunks grouped); C1's w = 100 is copy-bound
+        assert (st["lpt_from_chunk"] < st["input_chunks"]) == grouped, st
+        out = torch.zeros(24 * pairs.n_pairs, dtype=torch.uint8, device="cuda")
+        gpu_lib.align_batch(c, dev(pairs.ref), dev(pairs.ref_off.view(np.int64)), dev(pairs.qry),
+                            dev(pairs.qry_off.view(np.int64)), params, out=out)
+        assert gpu_lib.device_results(out).tobytes() == host.tobytes()
+        idx = np.arange(0, pairs.n_pairs, max(1, pairs.n_pairs // 12))
+        rc, exp, _ = oracle.align_batch(pairs.subset(idx), params)
+        assert rc == 0 and host[idx].tobytes() == exp.tobytes()
+    c.close()
+
+
 def test_kernel_selection(gpu_lib, ctx):
     """The 16-bit packed kernel runs for the paper's scoring at w = 500; parameters outside
     its exactness guard run the 32-bit kernel."""

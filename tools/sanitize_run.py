@@ -1,10 +1,13 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck): both kernels,
-the trace path, pack4 and plan on C1 pairs plus an edge corpus."""
+all three slot tiers (the edge corpus at w = 500 needs all of them), streamed host inputs
+in many chunks, the trace path, pack4 and plan on C1 pairs plus an edge corpus."""
 import os
 import sys
 
 import numpy as np
 import torch
+
+os.environ.setdefault("AGATHA_CHUNK_BYTES", "4096")  # many streamed chunks for host inputs
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
