@@ -1697,13 +1697,13 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   // flag.  Device inputs are one chunk that is ready from the start.
   int nchunks = 1;
   ctx->h_chunk_first[0] = 0;
+  // pinned mirror: ints [0..9] the scalars below, u64 [5] [6] the device inputs' total
+  // lengths (read with the plan's scalars: one host round trip), int [14] the final flags
+  uint64_t* h_tot = (uint64_t*)ctx->h_scalars + 5;
   if (dev_in) {
-    uint64_t tmp[2];
-    CUDA_TRY(cudaMemcpyAsync(&tmp[0], b->ref_off + P, 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(&tmp[1], b->qry_off + P, 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    tot_r = tmp[0];
-    tot_q = tmp[1];
+    CUDA_TRY(cudaMemcpyAsync(h_tot, b->ref_off + P, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(h_tot + 1, b->qry_off + P, 8, cudaMemcpyDeviceToHost, st));
+    tot_r = tot_q = 0;  // known after the plan's synchronisation
     d_ref = b->ref; d_qry = b->qry; d_roff = b->ref_off; d_qoff = b->qry_off;
   } else {
     tot_r = b->ref_off[P];
@@ -1760,8 +1760,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes64, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)P, 0, 40, st);
   if (sort_bytes64 > sort_bytes) sort_bytes = sort_bytes64;
-  if ((rc = grow(ctx->rw, 4 * (tot_r / 8 + 4 * P + 4))) || (rc = grow(ctx->qw, 4 * (tot_q / 8 + 4 * P + 4))) ||
-      (rc = grow(ctx->nominal, 4 * P)) || (rc = grow(ctx->nominal_sorted, 4 * P)) ||
+  if ((rc = grow(ctx->nominal, 4 * P)) || (rc = grow(ctx->nominal_sorted, 4 * P)) ||
       (rc = grow(ctx->iota, 4 * P)) || (rc = grow(ctx->order, 4 * P)) || (rc = grow(ctx->bad, P)) ||
       (rc = grow(ctx->sort_tmp, sort_bytes)) || (rc = grow(ctx->scalars, 64)) ||
       (rc = grow(ctx->chunk_first, 8 * (kMaxChunks + 1))) || (rc = grow(ctx->chunk_of, P)) ||
@@ -1819,6 +1818,13 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   const int err0 = ctx->h_scalars[0], maxD = ctx->h_scalars[1], maxoff16 = ctx->h_scalars[3];
   const int tier_n[3] = {ctx->h_scalars[4], ctx->h_scalars[5], ctx->h_scalars[6]};
   const int maxoff16_t0 = ctx->h_scalars[7];
+  if (dev_in) {
+    tot_r = h_tot[0];
+    tot_q = h_tot[1];
+  }
+  // packed sequences: guard word + data + guard word per pair (load_word_rw)
+  if ((rc = grow(ctx->rw, 4 * (tot_r / 8 + 4 * P + 4))) || (rc = grow(ctx->qw, 4 * (tot_q / 8 + 4 * P + 4))))
+    return rc;
   if (err0 & 2) return AGATHA_EEMPTY;
   if (err0 & 4) return AGATHA_ERANGE;
   CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
@@ -1930,10 +1936,10 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   if (!dev_out)
     CUDA_TRY(cudaMemcpyAsync(out, d_out, sizeof(agatha_result_t) * P, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaEventRecord(ctx->ev[4], st));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars + 14, d_sc, 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (!dev_in) CUDA_TRY(cudaStreamSynchronize(ctx->copy_stream));
-  CUDA_TRY(cudaMemcpy(ctx->h_scalars, d_sc, 4, cudaMemcpyDeviceToHost));
-  if (ctx->h_scalars[0] & 1) return AGATHA_ECHAR;  // set by the fused pack (a1)
+  if (ctx->h_scalars[14] & 1) return AGATHA_ECHAR;  // set by the fused pack (a1)
   if (dev_in) cudaEventElapsedTime(&ctx->stats.h2d_ms, ctx->ev[0], ctx->ev[1]);
   else cudaEventElapsedTime(&ctx->stats.h2d_ms, ctx->cev[0], ctx->cev[1]);
   cudaEventElapsedTime(&ctx->stats.prep_ms, ctx->ev[1], ctx->ev[2]);
