@@ -1599,7 +1599,7 @@ void score_table16(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
 }
 
 template <int NREG, bool TRACE, int NCAP>
-int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
+int occupancy16() {  // resident blocks per SM
   static int occ = -1;
   if (occ < 0) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align16_kernel<NREG, TRACE, NCAP>,
@@ -1609,6 +1609,19 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
     }
     if (occ < 1) occ = 1;
   }
+  return occ;
+}
+
+// warps (pairs in flight) of the persistent grid of slot tier t
+long long warp_slots16(const agatha_ctx* ctx, int t) {
+  const int occ = t == 0 ? occupancy16<16, false, 8>() * Front16<16>::wpb
+                : (t == 1 ? occupancy16<8, false, 8>() * Front16<8>::wpb : occupancy16<4, false, 3>() * Front16<4>::wpb);
+  return (long long)ctx->num_sms * occ;
+}
+
+template <int NREG, bool TRACE, int NCAP>
+int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
+  const int occ = occupancy16<NREG, TRACE, NCAP>();
   const long long want = (long long)ctx->num_sms * occ;
   constexpr int wpb = Front16<NREG>::wpb;
   const long long need = ((long long)A.n_pairs + wpb - 1) / wpb;
@@ -1801,17 +1814,6 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   CUDA_TRY(cudaGetLastError());
   int launches = 1, lib_launches = 0;
   const uint32_t* d_order = (const uint32_t*)ctx->iota.p;
-  if (!(b->flags & AGATHA_ORDER_INPUT)) {
-    // a2: longest first within each input chunk (chunk-major) within each slot tier
-    // (tier-major): key = (tier << (32 + chunk_bits)) | (chunk << 32) | ~nominal
-    const int end_bit = 32 + chunk_bits + 2;
-    size_t tb = ctx->sort_tmp.cap;
-    CUDA_TRY(cub::DeviceRadixSort::SortPairs(
-        ctx->sort_tmp.p, tb, (const uint64_t*)ctx->key64.p, (uint64_t*)ctx->key64_sorted.p,
-        (const uint32_t*)ctx->iota.p, (uint32_t*)ctx->order.p, (int)P, 0, end_bit, st));
-    d_order = (const uint32_t*)ctx->order.p;
-    lib_launches = 4;
-  }
   // K (slots per lane) from the widest band in the batch
   CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 40, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -1827,6 +1829,34 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     return rc;
   if (err0 & 2) return AGATHA_EEMPTY;
   if (err0 & 4) return AGATHA_ERANGE;
+
+  const int K = maxD <= 512 ? 16 : 32;
+  const bool k16 = use16(p, maxD) && !(b->flags & AGATHA_FORCE_32BIT);
+  const bool tr = trace_pair >= 0;
+  // Slot tiers (DESIGN.md §6.1): each pair runs at the narrowest front that holds its
+  // band, one persistent launch per non-empty tier on its own stream, so the narrow
+  // tiers fill the SMs as the wide tier's blocks retire.  The order is tier-major, so
+  // tier t's pairs are a contiguous range of it.  One launch (the widest front the batch
+  // needs) in input order, with a shared queue, or when tracing.
+  const bool split = k16 && !tr && !b->queue && !(b->flags & (AGATHA_ORDER_INPUT | AGATHA_SINGLE_TIER));
+  bool sort = !(b->flags & AGATHA_ORDER_INPUT);
+  if (sort && k16 && !b->queue) {
+    // one launch whose persistent warps take every pair at once: the order is moot
+    const int t = tier_of(maxD);
+    const bool one = !split || (tier_n[0] > 0) + (tier_n[1] > 0) + (tier_n[2] > 0) == 1;
+    if (one && (long long)P <= warp_slots16(ctx, t)) sort = false;
+  }
+  if (sort) {
+    // a2: longest first within each input chunk group (chunk-major) within
+    // each slot tier (tier-major): key = (tier << (32 + chunk_bits)) | (group << 32) | ~nominal
+    const int end_bit = 32 + chunk_bits + 2;
+    size_t tb = ctx->sort_tmp.cap;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(
+        ctx->sort_tmp.p, tb, (const uint64_t*)ctx->key64.p, (uint64_t*)ctx->key64_sorted.p,
+        (const uint32_t*)ctx->iota.p, (uint32_t*)ctx->order.p, (int)P, 0, end_bit, st));
+    d_order = (const uint32_t*)ctx->order.p;
+    lib_launches = 4;
+  }
   CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
 
   AlignArgs A;
@@ -1868,15 +1898,6 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     CUDA_TRY(cudaEventRecord(ctx->cev[1], ctx->copy_stream));
   }
   int grid = 0;
-  const int K = maxD <= 512 ? 16 : 32;
-  const bool k16 = use16(p, maxD) && !(b->flags & AGATHA_FORCE_32BIT);
-  const bool tr = trace_pair >= 0;
-  // Slot tiers (DESIGN.md §6.1): each pair runs at the narrowest front that holds its
-  // band, one persistent launch per non-empty tier on its own stream, so the narrow
-  // tiers fill the SMs as the wide tier's blocks retire.  The order is tier-major, so
-  // tier t's pairs are a contiguous range of it.  One launch (the widest front the batch
-  // needs) in input order, with a shared queue, or when tracing.
-  const bool split = k16 && !tr && !b->queue && !(b->flags & (AGATHA_ORDER_INPUT | AGATHA_SINGLE_TIER));
   int tiers_launched = 0, slots = 0;
   memset(ctx->stats.tier_pairs, 0, sizeof(ctx->stats.tier_pairs));
   if (split) {
