@@ -64,7 +64,9 @@ def test_random_short_pairs(gpu_lib, ctx, kflags, band):
                                    (504, 504), (503, 504), (500, 500), (300, 292), (511, 511),
                                    (511, 500), (0, 600), (600, 0), (264, 264),
                                    # NREG = 4 (the narrow slot tier, D <= 256): off = 0..3
-                                   (127, 128), (127, 127), (126, 127), (126, 126), (64, 64)])
+                                   (127, 128), (127, 127), (126, 127), (126, 126), (64, 64),
+                                   # slot-tier boundaries: D = 257 (NREG 8), 513 (NREG 16)
+                                   (128, 128), (256, 256)])
 def test_band_layouts_long_pairs(gpu_lib, ctx, bl, br):
     rng = np.random.default_rng(7000 + bl * 1000 + br)
     lst = []
