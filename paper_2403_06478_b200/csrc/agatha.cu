@@ -1913,20 +1913,20 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
       cudaStream_t ts = st;
       if (t > 0) {
         ts = ctx->tier_stream[t - 1];
-        CUDA_TRY(cudaStreamWaitEvent(ts, ctx->tev[0], 0));
+        if (cudaStreamWaitEvent(ts, ctx->tev[0], 0) != cudaSuccess) { rc = AGATHA_ECUDA; break; }
       }
       int g = 0;
       if (t == 0) rc = launch_align16_wide(ctx, At, ts, &g, maxoff16_t0);
       else if (t == 1) rc = launch_align16<8, false, 8>(ctx, At, ts, &g);
       else rc = launch_align16<4, false, 3>(ctx, At, ts, &g);
-      if (t > 0) CUDA_TRY(cudaEventRecord(ctx->tev[t], ts));
+      if (t > 0 && !rc && cudaEventRecord(ctx->tev[t], ts) != cudaSuccess) rc = AGATHA_ECUDA;
       grid += g;
       ++tiers_launched;
       ctx->stats.tier_pairs[t] = tier_n[t];
       if (!slots) slots = 32 >> t;
     }
-    for (int t = 1; t < 3; ++t)
-      if (tier_n[t]) CUDA_TRY(cudaStreamWaitEvent(st, ctx->tev[t], 0));
+    for (int t = 1; t < 3 && !rc; ++t)
+      if (tier_n[t] && cudaStreamWaitEvent(st, ctx->tev[t], 0) != cudaSuccess) rc = AGATHA_ECUDA;
   } else if (k16) {
     // (NREG = 16) eight capped registers suffice when every pair's low padding
     // off = (-D) mod 16 is at most 8 (prep_kernel's max); else all sixteen
@@ -1948,7 +1948,9 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     slots = K;
   }
   ctx->stats.packed16 = k16 ? 1 : 0;
-  if (rc) {
+  if (rc) {  // nothing launched may still be using the caller's buffers on return
+    cudaStreamSynchronize(st);
+    for (int i = 0; i < 2; ++i) cudaStreamSynchronize(ctx->tier_stream[i]);
     if (!dev_in) cudaStreamSynchronize(ctx->copy_stream);
     return rc;
   }
