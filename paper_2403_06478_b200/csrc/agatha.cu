@@ -792,7 +792,10 @@ constexpr int kW16 = -29250;       // "-infinity" (walls, E/F of boundary cells)
 constexpr int kCapNeg16 = -21250;  // padding cap
 constexpr int kEmpty16 = -17250;   // lane max at or below: no valid cell on the anti-diagonal
 constexpr int kTop16 = -129;       // every stored H is at most this
-constexpr int kRebase16 = 32;      // iterations (64 anti-diagonals) between re-centrings
+#ifndef AGATHA_REBASE16
+#define AGATHA_REBASE16 32
+#endif
+constexpr int kRebase16 = AGATHA_REBASE16;  // iterations (2x anti-diagonals) between re-centrings
 
 __device__ __forceinline__ uint32_t pack2(int lo, int hi) {
   return ((uint32_t)lo & 0xFFFFu) | ((uint32_t)hi << 16);
@@ -1562,7 +1565,7 @@ void score_table(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
 // stays in (kEmpty16, kTop16] and every wall/cap value above -32768.
 static long long drift16(const agatha_params_t* p) {
   const long long mx = std::max<long long>(p->match, std::max<long long>(p->mismatch, p->ambig));
-  return 70 * (2 * (long long)p->gap_open + mx);
+  return (2 * kRebase16 + 6) * (2 * (long long)p->gap_open + mx);  // 70 at 32 iterations
 }
 // Cells outside the table may rise above the anti-diagonal max of the valid cells by at
 // most (alpha - beta) per anti-diagonal for as long as they stay outside (at most
