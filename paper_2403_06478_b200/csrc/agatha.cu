@@ -1352,9 +1352,15 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 #ifndef AGATHA_MINB16
 #define AGATHA_MINB16 3
 #endif
+#ifndef AGATHA_MINB8
+#define AGATHA_MINB8 4
+#endif
+#ifndef AGATHA_MINB4
+#define AGATHA_MINB4 4
+#endif
 template <int NREG> struct Front16 {
   static constexpr int wpb = NREG >= 16 ? AGATHA_WPB16 : 4;
-  static constexpr int minb = NREG >= 16 ? AGATHA_MINB16 : (NREG >= 8 ? 4 : 5);
+  static constexpr int minb = NREG >= 16 ? AGATHA_MINB16 : (NREG >= 8 ? AGATHA_MINB8 : AGATHA_MINB4);
 };
 
 template <int NREG, bool TRACE, int NCAP>
