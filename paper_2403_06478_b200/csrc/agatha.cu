@@ -48,6 +48,10 @@ constexpr int kMaxWarpsWide = 4;        // wide-band tier: up to 4 warps per pai
 constexpr int kMaxSlotsWide = kMaxWarpsWide * kMaxSlots;
 constexpr int kMaxChunks = 255;         // input chunks of one call (chunk ids are uint8)
 constexpr uint64_t kChunkBytes = 48ull << 20;  // target ASCII bytes per streamed chunk
+constexpr int kRampChunks = 5;                  // the first chunks start at 1/32 of it
+#ifndef AGATHA_CHUNK_RAMP
+#define AGATHA_CHUNK_RAMP 1
+#endif
 
 struct AlignArgs {
   uint32_t* rw;              // packed R words, pair p's region starts at word (ref_off[p] >> 3) + 4p
@@ -1741,13 +1745,25 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     d_qoff = (const uint64_t*)ctx->qry_off.p;
     uint64_t target = ctx->chunk_bytes;
     const uint64_t total = tot_r + tot_q;
-    if (total / target + 2 > (uint64_t)kMaxChunks) target = total / (kMaxChunks - 2) + 1;
+    if (total / target + 2 + kRampChunks > (uint64_t)kMaxChunks)
+      target = total / (kMaxChunks - 2 - kRampChunks) + 1;
+    // the first chunks ramp up from target / 2^kRampChunks, doubling: the kernel starts
+    // on the first pairs after a short copy instead of a full chunk's
+    // (a batch under one chunk stays one chunk: small copies cost more in API calls
+    // than they save in latency, measured on C1)
+#if AGATHA_CHUNK_RAMP
+    uint64_t cur = total <= target ? target
+                                   : std::max<uint64_t>(target >> kRampChunks, std::min<uint64_t>(target, 64u << 10));
+#else
+    uint64_t cur = target;
+#endif
     uint64_t acc = 0;
     for (uint64_t k = 0; k < P; ++k) {
       acc += (b->ref_off[k + 1] - b->ref_off[k]) + (b->qry_off[k + 1] - b->qry_off[k]);
-      if (acc >= target && k + 1 < P) {
+      if (acc >= cur && k + 1 < P) {
         ctx->h_chunk_first[nchunks++] = k + 1;
         acc = 0;
+        cur = std::min(2 * cur, target);
       }
     }
   }
