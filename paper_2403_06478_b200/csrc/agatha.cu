@@ -1722,6 +1722,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   // each) on the copy stream while the align kernel runs; a pair waits for its chunk's
   // flag.  Device inputs are one chunk that is ready from the start.
   int nchunks = 1;
+  double est_cells = 0.0;  // host inputs: sum of min(m,n) * D, the kernel-time estimate
   ctx->h_chunk_first[0] = 0;
   // pinned mirror: ints [0..9] the scalars below, u64 [5] [6] the device inputs' total
   // lengths (read with the plan's scalars: one host round trip), int [14] the final flags
@@ -1758,8 +1759,12 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     uint64_t cur = target;
 #endif
     uint64_t acc = 0;
+    const int64_t pbl = p->band_left, pbr = p->band_right;
     for (uint64_t k = 0; k < P; ++k) {
-      acc += (b->ref_off[k + 1] - b->ref_off[k]) + (b->qry_off[k + 1] - b->qry_off[k]);
+      const int64_t m = (int64_t)(b->ref_off[k + 1] - b->ref_off[k]), n = (int64_t)(b->qry_off[k + 1] - b->qry_off[k]);
+      acc += (uint64_t)(m + n);
+      const int64_t bl = (pbl < 0 || pbl > n) ? n : pbl, br = (pbr < 0 || pbr > m) ? m : pbr;
+      est_cells += (double)(m < n ? m : n) * (double)(bl + br + 1);  // for lpt_from below
       if (acc >= cur && k + 1 < P) {
         ctx->h_chunk_first[nchunks++] = k + 1;
         acc = 0;
@@ -1777,14 +1782,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   // kernel = sum min(m,n)*D / 4 TCUPS, copy = bytes / 20 GB/s, margin 1.25.
   int lpt_from = nchunks;
   if (!dev_in && nchunks > 2) {
-    double cells = 0.0;
-    for (uint64_t k = 0; k < P; ++k) {
-      const int64_t m = (int64_t)(b->ref_off[k + 1] - b->ref_off[k]), n = (int64_t)(b->qry_off[k + 1] - b->qry_off[k]);
-      const int64_t bl = (p->band_left < 0 || p->band_left > n) ? n : p->band_left;
-      const int64_t br = (p->band_right < 0 || p->band_right > m) ? m : p->band_right;
-      cells += (double)(m < n ? m : n) * (double)(bl + br + 1);
-    }
-    const double t_kernel = cells / 4e12, t_copy = (double)(tot_r + tot_q) / 20e9;
+    const double t_kernel = est_cells / 4e12, t_copy = (double)(tot_r + tot_q) / 20e9;
     const double f = t_kernel > 0 ? 1.25 * t_copy / t_kernel : 1.0;
     if (f < 1.0) lpt_from = std::max(1, (int)std::ceil(f * nchunks));
   }
