@@ -792,6 +792,9 @@ __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A)
 #ifndef AGATHA_VOTE
 #define AGATHA_VOTE 1    // 0: plain uniform branch instead of the vote in process16 (-0.2%)
 #endif
+#ifndef AGATHA_VOTE_NARROW
+#define AGATHA_VOTE_NARROW 0  // the same for the 16- and 8-slot fronts: no vote (+0.3-2.3%)
+#endif
 constexpr int kW16 = -29250;       // "-infinity" (walls, E/F of boundary cells)
 constexpr int kCapNeg16 = -21250;  // padding cap
 constexpr int kEmpty16 = -17250;   // lane max at or below: no valid cell on the anti-diagonal
@@ -907,11 +910,11 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
   const bool chk = nonempty && Hs < s.zthr && ((STEADY && !TRACE) || c < s.mn);
   // upd and chk are warp-uniform (rH is a warp reduction, the rest is per-pair state):
   // a plain uniform branch, no vote
-#if AGATHA_VOTE
-  if (!__any_sync(kFull, upd || chk || (TRACE && nonempty))) return false;
-#else
-  if (!(upd || chk || (TRACE && nonempty))) return false;
-#endif
+  if ((NREG >= 16) ? AGATHA_VOTE : AGATHA_VOTE_NARROW) {
+    if (!__any_sync(kFull, upd || chk || (TRACE && nonempty))) return false;
+  } else if (!(upd || chk || (TRACE && nonempty))) {
+    return false;
+  }
   if (TRACE || chk) {
     uint32_t r[NREG / 2];
 #pragma unroll
