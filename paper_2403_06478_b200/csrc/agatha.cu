@@ -778,6 +778,9 @@ __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A)
 #ifndef AGATHA_RREUSE
 #define AGATHA_RREUSE 0  // 1: carry the PAR = 1 R shift into the next PAR = 0 step (-1.6%)
 #endif
+#ifndef AGATHA_RREUSE_NARROW
+#define AGATHA_RREUSE_NARROW 1  // the same for the 16- and 8-slot fronts (+0.5-0.8%)
+#endif
 #ifndef AGATHA_LMSHL
 #define AGATHA_LMSHL 1  // lane max of the two halves via lm << 16 (IMAD) instead of hi16_fma
 #endif
@@ -1192,6 +1195,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   // The R window shifted for the PAR = 1 step (4*oR + 4) is the next iteration's PAR = 0
   // shift (oR advances by one), also across a refill: the clamped shift by 32 returns
   // the second word, which the refill makes the first.
+  constexpr bool kRReuse = NREG >= 16 ? AGATHA_RREUSE : AGATHA_RREUSE_NARROW;
   uint32_t rsc[2] = {0u, 0u};
   rshift(rsc, 4 * oR);
   auto iteration = [&](auto masked_tag) {
@@ -1208,12 +1212,12 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 #endif
     // ---- step PAR = 0, anti-diagonal cb ----
     {
-#if AGATHA_RREUSE
-      scores(S2, rsc, qg);
-#else
-      rshift(rs, 4 * oR);
-      scores(S2, rs, qg);
-#endif
+      if (kRReuse) {
+        scores(S2, rsc, qg);
+      } else {
+        rshift(rs, 4 * oR);
+        scores(S2, rs, qg);
+      }
       int tlo = 0, thi = NC;
       if (MASKED) {
         const int ib = u + lane * NC, jb = u - dls - lane * NC;
@@ -1238,10 +1242,10 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       rshift(rs, 4 * oR + 4);
       scores(S2, rs, qg);
 #endif
-#if AGATHA_RREUSE
-      rsc[0] = rs[0];
-      rsc[1] = rs[1];
-#endif
+      if (kRReuse) {
+        rsc[0] = rs[0];
+        rsc[1] = rs[1];
+      }
       int tlo = 0, thi = NC;
       if (MASKED) {
         const int ib = u + 1 + lane * NC, jb = u - dls - lane * NC;
