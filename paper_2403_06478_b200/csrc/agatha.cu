@@ -1363,6 +1363,10 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 #ifndef AGATHA_MINB16
 #define AGATHA_MINB16 3
 #endif
+// NREG = 8: off = (-D) mod 8 <= 7, so seven capped registers always cover the padding
+#ifndef NCAP8
+#define NCAP8 7
+#endif
 #ifndef AGATHA_MINB8
 #define AGATHA_MINB8 4
 #endif
@@ -1635,7 +1639,7 @@ int occupancy16() {  // resident blocks per SM
 // warps (pairs in flight) of the persistent grid of slot tier t
 long long warp_slots16(const agatha_ctx* ctx, int t) {
   const int occ = t == 0 ? occupancy16<16, false, 8>() * Front16<16>::wpb
-                : (t == 1 ? occupancy16<8, false, 8>() * Front16<8>::wpb : occupancy16<4, false, 3>() * Front16<4>::wpb);
+                : (t == 1 ? occupancy16<8, false, NCAP8>() * Front16<8>::wpb : occupancy16<4, false, 3>() * Front16<4>::wpb);
   return (long long)ctx->num_sms * occ;
 }
 
@@ -1947,7 +1951,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
       }
       int g = 0;
       if (t == 0) rc = launch_align16_wide(ctx, At, ts, &g, maxoff16_t0);
-      else if (t == 1) rc = launch_align16<8, false, 8>(ctx, At, ts, &g);
+      else if (t == 1) rc = launch_align16<8, false, NCAP8>(ctx, At, ts, &g);
       else rc = launch_align16<4, false, 3>(ctx, At, ts, &g);
       if (t > 0 && !rc && cudaEventRecord(ctx->tev[t], ts) != cudaSuccess) rc = AGATHA_ECUDA;
       grid += g;
@@ -1962,7 +1966,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     // off = (-D) mod 16 is at most 8 (prep_kernel's max); else all sixteen
     const int t = tier_of(maxD);
     if (t == 2) rc = tr ? launch_align16<4, true, 3>(ctx, A, st, &grid) : launch_align16<4, false, 3>(ctx, A, st, &grid);
-    else if (t == 1) rc = tr ? launch_align16<8, true, 8>(ctx, A, st, &grid) : launch_align16<8, false, 8>(ctx, A, st, &grid);
+    else if (t == 1) rc = tr ? launch_align16<8, true, NCAP8>(ctx, A, st, &grid) : launch_align16<8, false, NCAP8>(ctx, A, st, &grid);
     else if (tr) rc = launch_align16<16, true, 16>(ctx, A, st, &grid);
     else rc = launch_align16_wide(ctx, A, st, &grid, maxoff16);
     tiers_launched = 1;
