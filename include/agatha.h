@@ -90,8 +90,9 @@ typedef struct {
   int32_t* queue; /* NULL: the context's own pair counter.  Otherwise a shared counter
                      from agatha_queue_create/_open (cross-GPU dynamic balancing, SURVEY.md
                      §8(f) NEXT #1): every participant aligns the SAME batch with the same
-                     params; its persistent kernel claims pairs (in the common longest-first
-                     order) from this counter with system-scope atomics, aligns only those,
+                     params; its persistent kernels claim pairs (in the common tier-major,
+                     longest-first order; one counter per slot tier at queue[0..2]) with
+                     system-scope atomics, align only those,
                      and writes only their result rows; all other rows of `out` are
                      zero-filled.  The caller resets the counter (agatha_queue_reset)
                      before the participants start and merges their outputs (each row is
@@ -162,10 +163,11 @@ int agatha_localmax_trace(agatha_ctx_t* ctx, const agatha_batch_t* batch,
                           const agatha_params_t* params, uint64_t pair, int32_t* score,
                           int32_t* ref_i, int64_t cap, void* cuda_stream);
 
-/* NEXT #1: a shared pair counter for agatha_batch_t.queue.  _create allocates a zeroed
- * device counter on the context's device and returns its CUDA IPC handle (64 bytes) for
- * other processes; _open maps a handle from another process (peer access over NVLink
- * when on another GPU) into this context; _reset zeroes a counter on `cuda_stream`;
+/* NEXT #1: a shared pair counter for agatha_batch_t.queue.  _create allocates zeroed
+ * device counters (four int32, one per slot tier) on the context's device and returns
+ * their CUDA IPC handle (64 bytes) for other processes; _open maps a handle from another
+ * process (peer access over NVLink when on another GPU) into this context; _reset zeroes
+ * the counters on `cuda_stream`;
  * _close releases a created (opened = 0) or opened (opened = 1) counter. */
 int agatha_queue_create(agatha_ctx_t* ctx, int32_t** queue, uint8_t handle[64]);
 int agatha_queue_open(agatha_ctx_t* ctx, const uint8_t handle[64], int32_t** queue);

@@ -1871,8 +1871,8 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   // band, one persistent launch per non-empty tier on its own stream, so the narrow
   // tiers fill the SMs as the wide tier's blocks retire.  The order is tier-major, so
   // tier t's pairs are a contiguous range of it.  One launch (the widest front the batch
-  // needs) in input order, with a shared queue, or when tracing.
-  const bool split = k16 && !tr && !b->queue && !(b->flags & (AGATHA_ORDER_INPUT | AGATHA_SINGLE_TIER));
+  // needs) in input order or when tracing.
+  const bool split = k16 && !tr && !(b->flags & (AGATHA_ORDER_INPUT | AGATHA_SINGLE_TIER));
   bool sort = !(b->flags & AGATHA_ORDER_INPUT);
   if (sort && k16 && !b->queue) {
     // one launch whose persistent warps take every pair at once: the order is moot
@@ -1942,7 +1942,9 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
       AlignArgs At = A;
       At.order = d_order + start;
       At.n_pairs = (uint32_t)tier_n[t];
-      At.queue = t == 0 ? d_sc + 2 : d_sc + 7 + t;
+      // a shared queue (NEXT #1) holds one counter per tier, claimed in the same
+      // tier-major order by every participant
+      At.queue = b->queue ? b->queue + t : (t == 0 ? d_sc + 2 : d_sc + 7 + t);
       start += (uint32_t)tier_n[t];
       cudaStream_t ts = st;
       if (t > 0) {
@@ -2220,7 +2222,7 @@ int agatha_queue_open(agatha_ctx_t* ctx, const uint8_t handle[64], int32_t** que
 int agatha_queue_reset(agatha_ctx_t* ctx, int32_t* queue, void* stream) {
   if (!ctx || !queue) return AGATHA_EINVAL;
   CUDA_TRY(cudaSetDevice(ctx->device));
-  CUDA_TRY(cudaMemsetAsync(queue, 0, sizeof(int32_t), (cudaStream_t)stream));
+  CUDA_TRY(cudaMemsetAsync(queue, 0, 4 * sizeof(int32_t), (cudaStream_t)stream));  // one per slot tier
   return AGATHA_OK;
 }
 

@@ -441,9 +441,10 @@ def _merge_rows(*outs):
     return acc.view(oracle.RESULT_DTYPE)
 
 
-def test_shared_queue_two_contexts(gpu_lib, ctx):
+@pytest.mark.parametrize("name", ["C5", "LS10"])  # LS10: two slot tiers, one counter each
+def test_shared_queue_two_contexts(gpu_lib, ctx, name):
     import threading
-    cfg = synth.CONFIGS["C5"]
+    cfg = synth.CONFIGS[name]
     pairs = synth.generate(cfg, 0, 600)
     params = vars(cfg.scoring)
     full = gpu_lib.align_pairs(ctx, pairs, params)
@@ -468,6 +469,8 @@ def test_shared_queue_two_contexts(gpu_lib, ctx):
             claimed = [int((o["cells"] != 0).sum()) for o in outs]
             assert sum(claimed) == pairs.n_pairs, claimed
             assert _merge_rows(*outs).tobytes() == full.tobytes()
+            if name == "LS10":
+                assert ctx.stats()["tier_pairs"][1] > 0 and ctx.stats()["tier_pairs"][0] > 0
     finally:
         q.close()
         c2.close()
