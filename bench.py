@@ -17,8 +17,13 @@ configs[1] (C2: 100k HiFi-like pairs of 10-20 kbp, 1% error, band 500, Z-drop 40
                  on the host cores (rank 0 only).
 
 ``--impl reference`` times the oracle itself (the reference arm of this tier).
-Multi-GPU (torchrun): each rank aligns its own shard of pairs (weak scaling: per-GPU
-work fixed), results are gathered with NCCL all_gather; time = max over ranks.
+Multi-GPU: ``--gpus N`` (N > 1) without a torchrun environment re-launches this script
+under ``torch.distributed.run`` with N ranks (one per GPU, 127.0.0.1 rendezvous); with
+fewer than N visible GPUs it fails instead of running a smaller job.  The batch is split
+by a deterministic LPT partition over nominal cells; ``--scaling weak``
+(default: N x the config's pairs, the per-GPU work fixed) or ``strong`` (the config's
+fixed batch split N ways, BASELINE.json configs[4]).  Results are gathered with one NCCL
+all_gather (shards padded to the largest); time = max over ranks.
 """
 from __future__ import annotations
 
@@ -48,15 +53,27 @@ OPS_PER_CELL = 2.25
 OPS_PER_CELL_32 = 4.5
 SM_COUNT = 148
 LANES_PER_CLK_PER_SM = 64
-# dram__bytes_read.sum + dram__bytes_write.sum per align launch on the full C2 batch, from
-# one ncu capture (profiles/r01c_ncu_align16_dram_c2.csv, r01_ncu_align_kernel_summary.csv);
-# updated per profile.
-TRAFFIC = {"align_kernel<32>": 1.603e9 + 0.0748e9, "align16_kernel<16>": 3.328e9 + 1.545e9}
+# SURVEY.md §8(d) roofline: I_cell = 9 int32 lane-instructions per cell (Eq. 1-3 + Eq. 5 on
+# sm_100a) against the measured integer lane-instruction rate P_int; the .S16x2 datapath
+# the 16-bit kernel runs carries two cells per lane-instruction, so its peak counts two
+# int16 lane-ops per lane-instruction (stated in the line).  P_int measured on the B200:
+# VIADDMNMX/VIMNMX3 .S16x2 62.4 lanes/clk/SM (profiles/r01_dpx16.jsonl).
+I_CELL = 9
+P_INT_LANES_PER_CLK_PER_SM = 62.4
+PAPER_SPEEDUP = {"value": 18.8, "what": "AGAThA vs minimap2 extension (geometric mean over 9 datasets)",
+                 "gpu": "NVIDIA RTX A6000", "cpu": "AMD EPYC 7313P 16C/32T, minimap2 SSE4.1",
+                 "cite": "PAPER.md l.600-602 (setup), l.673 (18.8x), l.830 (16C32T SSE4)",
+                 "note": "the paper's CPU side is an optimised SIMD aligner, not a plain oracle: "
+                         "not comparable like for like with cpu_baseline"}
 
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="ranks (one per GPU); default 1, or the torchrun world size")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: N x the config's pairs (per-GPU work fixed); strong: the "
+                         "config's batch split over the N ranks")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -129,6 +146,89 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def launch_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: re-run this script with N ranks on this node (the
+    driver's own launch line), after checking that N GPUs are visible."""
+    import socket
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+              file=sys.stderr, flush=True)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def newest_profile(pattern: str):
+    """The newest committed profile matching profiles/<pattern> (round tags sort by name)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", pattern)))
+    return files[-1] if files else None
+
+
+def ncu_kernel_metrics(path: str, kernel_substr: str):
+    """{metric: value} of the first launch of a kernel in an `ncu --csv` metrics file, or of
+    a tools/ncu_summary.py summary (metric,unit,value)."""
+    import csv
+
+    out = {}
+    with open(path) as f:
+        rows = [r for r in csv.reader(f) if r]
+    if rows and rows[0][:3] == ["metric", "unit", "value"]:
+        for r in rows[1:]:
+            if len(r) == 3:
+                try:
+                    out[r[0]] = float(r[2])
+                except ValueError:
+                    pass
+        return out
+    hdr = next((i for i, r in enumerate(rows) if "Metric Name" in r), None)
+    if hdr is None:
+        return out
+    h = rows[hdr]
+    ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    first = None
+    for r in rows[hdr + 1:]:
+        if len(r) < len(h) or kernel_substr not in r[ki]:
+            continue
+        first = r[ii] if first is None else first
+        if r[ii] == first:
+            try:
+                out[r[mi]] = float(r[vi].replace(",", ""))
+            except ValueError:
+                pass
+    return out
+
+
+def cpu_info():
+    model, smt = None, None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        with open("/sys/devices/system/cpu/smt/active") as f:
+            smt = f.read().strip() == "1"
+    except OSError:
+        pass
+    return {"cpu_model": model, "smt": smt, "logical_cpus": os.cpu_count()}
+
+
 def cpu_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -136,13 +236,13 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
-def run_oracle_sample(pairs: synth.Pairs, params: dict, stride: int):
+def run_oracle_sample(pairs: synth.Pairs, params: dict, stride: int, threads: int = 0):
     """The oracle, as it stands, on every `stride`-th pair; returns (idx, results, seconds)."""
     import oracle
     idx = np.arange(0, pairs.n_pairs, stride)
     sub = pairs.subset(idx)
     t0 = time.perf_counter()
-    rc, res, _ = oracle.align_batch(sub, params, threads=cpu_cores())
+    rc, res, _ = oracle.align_batch(sub, params, threads=threads or cpu_cores())
     dt = time.perf_counter() - t0
     assert rc == 0, rc
     return idx, res, dt
@@ -171,17 +271,20 @@ def reference_arm(args, cfg, rank, world):
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": config_dict(cfg, n, world),
-        "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": cpu_cores(), "kind": "oracle",
-                         "sample": f"every {stride}th pair of {n} ({len(idx)} pairs per step)"},
+        "cpu_baseline": dict({"value": value, "unit": "GCUPS", "cores": cpu_cores(), "kind": "oracle",
+                              "sample": f"every {stride}th pair of {n} ({len(idx)} pairs per step)"},
+                             **cpu_info()),
+        "paper_speedup": PAPER_SPEEDUP,
         "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def config_dict(cfg, n_per_gpu, world):
+def config_dict(cfg, n_per_gpu, world, n_global=None):
     sc = cfg.scoring
     return {"workload": f"{cfg.name}: {cfg.description}", "pairs_per_gpu": n_per_gpu,
-            "global_pairs": n_per_gpu * world, "band": [sc.band_left, sc.band_right],
+            "global_pairs": n_per_gpu * world if n_global is None else n_global,
+            "band": [sc.band_left, sc.band_right],
             "zdrop": sc.zdrop,
             "scoring": {"match": sc.match, "mismatch": sc.mismatch, "ambig": sc.ambig,
                         "gap_open": sc.gap_open, "gap_extend": sc.gap_extend},
@@ -189,12 +292,46 @@ def config_dict(cfg, n_per_gpu, world):
             "l2": "inputs (GBs of sequence) exceed the 126 MB L2; no flush needed"}
 
 
+def rank_shard(full: synth.Config, world: int, rank: int, pinned_out=None):
+    """§8(e): the deterministic LPT partition of the global batch (full.n_pairs pairs of
+    the config's stream) over nominal cells; returns (shards, this rank's pairs).  Every
+    rank computes the same partition from the pair lengths alone and generates only its
+    own pairs (the generator is counter-based)."""
+    from paper_2403_06478_b200 import dist as adist
+
+    n_global = full.n_pairs
+    if world == 1:
+        return [np.arange(n_global, dtype=np.int64)], synth.generate(full, 0, n_global, pinned_out=pinned_out)
+    sc = full.scoring
+    rl, ql = synth.lengths(full, 0, n_global)
+    w = adist.nominal_cells(rl.astype(np.int64), ql.astype(np.int64), sc.band_left, sc.band_right)
+    shards = adist.lpt_partition(w, world)
+    return shards, synth.generate_idx(full, shards[rank], pinned_out=pinned_out)
+
+
+def stream_order(gathered, shards, n_global: int):
+    """Records all_gathered from the ranks (each shard padded to the largest; a uint8
+    tensor, CUDA or CPU) back into stream order on the host."""
+    from paper_2403_06478_b200 import dist as adist
+
+    rows = gathered.cpu().numpy().view(np.dtype([("score", "<i4"), ("ref_end", "<i4"), ("query_end", "<i4"),
+                                                  ("zdrop_antidiag", "<i4"), ("cells", "<i8")]))
+    return adist.scatter_gathered(rows, shards, n_global)
+
+
 def main():
     args = parse()
     cfg = synth.CONFIGS[args.config]
     rank, world, local = dist_env()
-    if args.impl == "reference":
+    if args.impl == "reference":  # the oracle on host cores: rank 0 only, no GPUs needed
         return reference_arm(args, cfg, rank, world)
+    if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1:
+        sys.exit(launch_ranks(args))
+    if args.gpus is None:
+        args.gpus = world
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but the launch has {world} rank(s)", file=sys.stderr)
+        sys.exit(2)
 
     import torch
     import torch.distributed as dist
@@ -203,29 +340,39 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's init log shows the communicator's rank count (nRanks) to the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = args.pairs or cfg.n_pairs
-    # rank r aligns pairs [r*n, (r+1)*n) of the config's infinite pair stream (weak scaling)
-    full = cfg.with_pairs(n * world)
+    sc = cfg.scoring
+    n_cfg = args.pairs or cfg.n_pairs
+    n_global = n_cfg * world if args.scaling == "weak" else n_cfg
+    full = cfg.with_pairs(n_global)
+    dynamic = args.balance == "dynamic"
 
     # pinned host buffers (used by the e2e leg); inputs copied once to HBM for `value`
     def pinned(nr, nq):
         return (torch.empty(nr, dtype=torch.uint8, pin_memory=True).numpy(),
                 torch.empty(nq, dtype=torch.uint8, pin_memory=True).numpy())
 
-    dynamic = args.balance == "dynamic"
     t0 = time.perf_counter()
-    # static: rank r holds its shard; dynamic: every rank holds the whole batch (replicated
-    # inputs) and claims chunks of it at run time
-    k0, k1 = (0, n * world) if dynamic else adist.shard_range(n, rank)
-    pairs = synth.generate(full, k0, k1, pinned_out=pinned)
+    if dynamic:
+        # every rank holds the whole batch (replicated inputs) and claims pairs at run time
+        shards = None
+        mine = np.arange(n_global, dtype=np.int64)
+        pairs = synth.generate(full, 0, n_global, pinned_out=pinned)
+    else:
+        shards, pairs = rank_shard(full, world, rank, pinned)
+        mine = shards[rank]
     gen_s = time.perf_counter() - t0
-    params = dict(vars(cfg.scoring))
+    params = dict(vars(sc))
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     d_ref, d_qry = dev(pairs.ref), dev(pairs.qry)
     d_roff, d_qoff = dev(pairs.ref_off.view(np.int64)), dev(pairs.qry_off.view(np.int64))
-    n_local = k1 - k0
-    d_out = torch.zeros(adist.RECORD_BYTES * n_local, dtype=torch.uint8, device="cuda")
+    n_local = pairs.n_pairs
+    pad = n_local if shards is None else max(len(x) for x in shards)
+    d_out_pad = torch.zeros(adist.RECORD_BYTES * pad, dtype=torch.uint8, device="cuda")
+    d_out = d_out_pad[:adist.RECORD_BYTES * n_local]
     flags = agatha.ORDER_INPUT if args.order == "input" else 0
     if args.tiers == "single":
         flags |= agatha.SINGLE_TIER
@@ -259,7 +406,7 @@ def main():
             state["mine"] = d_out.view(torch.int64).view(-1, 3)[:, 2].sum()
             adist.merge_claimed(d_out, world)  # NCCL all_reduce of the claimed rows
         elif world > 1:
-            adist.gather_results(d_out, world)  # NCCL all_gather of the 24-byte records
+            state["gathered"] = adist.gather_results(d_out_pad, world)  # NCCL all_gather
 
     def barrier():
         if world > 1:
@@ -290,24 +437,46 @@ def main():
     else:
         cells_rank = int(res["cells"].sum())
         cells_all = adist.sum_over_ranks(float(cells_rank), "cuda", world)
+    if not dynamic and world > 1:
+        res_all = stream_order(state["gathered"], shards, n_global)
+        assert res_all[mine].tobytes() == res.tobytes()
+        assert float(res_all["cells"].sum()) == cells_all
     sec = ms_max / 1e3
     gcups = cells_all * args.steps / sec / 1e9
-    aln_s = n * world * args.steps / sec
+    aln_s = n_global * args.steps / sec
+    launches_rank = state["launches"]
+    launches_all = int(adist.sum_over_ranks(float(launches_rank), "cuda", world))
 
-    # e2e: the public C ABI with pinned host buffers (H2D of inputs + D2H of results each step)
+    # e2e: the public C ABI with pinned host buffers: every step copies this rank's ASCII
+    # inputs in, aligns, (N > 1) gathers the records over NCCL, and reads the batch's result
+    # records back to the host (scattered into stream order at N > 1)
     e2e = None
     if not args.no_e2e:
         host_out = np.zeros(n_local, agatha.RESULT_DTYPE)
+        d_e2e_pad = torch.zeros_like(d_out_pad)
+        d_e2e = d_e2e_pad[:adist.RECORD_BYTES * n_local]
+        box = {}
 
         def e2e_step():
             if dynamic:
                 start_dynamic()
-            agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
-                               out=host_out, flags=flags, stream=stream, queue=queue)
-            if dynamic and world > 1:  # merge the ranks' claimed rows
-                t = torch.from_numpy(host_out.view(np.uint8)).cuda()
-                adist.merge_claimed(t, world)
-                host_out.view(np.uint8)[:] = t.cpu().numpy()
+                agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
+                                   out=host_out, flags=flags, stream=stream, queue=queue)
+                if world > 1:  # merge the ranks' claimed rows
+                    t = torch.from_numpy(host_out.view(np.uint8)).cuda()
+                    adist.merge_claimed(t, world)
+                    host_out.view(np.uint8)[:] = t.cpu().numpy()
+                box["res"] = host_out
+            elif world == 1:
+                agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
+                                   out=host_out, flags=flags, stream=stream)
+                box["res"] = host_out
+            else:
+                agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
+                                   out=d_e2e, flags=flags, stream=stream)
+                g = adist.gather_results(d_e2e_pad, world)
+                if rank == 0:
+                    box["res"] = stream_order(g, shards, n_global)
 
         e2e_step()
         barrier()
@@ -317,12 +486,23 @@ def main():
         ev1.record(stream)
         barrier()
         e_ms = adist.max_over_ranks(ev0.elapsed_time(ev1), "cuda", world)
-        assert host_out.tobytes() == res.tobytes()
+        if dynamic or world == 1:
+            assert box["res"].tobytes() == res.tobytes()
+            d2h = 24 * n_local
+        else:
+            if rank == 0:
+                assert box["res"][mine].tobytes() == res.tobytes()
+                assert box["res"].tobytes() == res_all.tobytes()
+            d2h = 24 * pad * world if rank == 0 else 0
         h2d = int(pairs.ref.nbytes + pairs.qry.nbytes + pairs.ref_off.nbytes + pairs.qry_off.nbytes)
+        h2d_all = int(adist.sum_over_ranks(float(h2d), "cuda", world))
         e2e = {"value": cells_all * args.steps / (e_ms / 1e3) / 1e9, "unit": "GCUPS",
-               "alignments_per_s": n * world * args.steps / (e_ms / 1e3),
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 24 * n_local,
+               "alignments_per_s": n_global * args.steps / (e_ms / 1e3),
+               "h2d_bytes_per_step": h2d_all, "d2h_bytes_per_step": d2h,
                "ms_per_step": e_ms / args.steps}
+        if world > 1:
+            e2e["h2d_bytes_per_step_rank0"] = h2d
+            e2e["gather"] = "NCCL all_gather of the 24-byte records (shards padded), then D2H on rank 0"
 
     if rank != 0:
         if world > 1:
@@ -334,56 +514,100 @@ def main():
     align_avg_ms = statistics.mean(align_ms)
     clocks = clk.summary()
     f_ghz = (clocks["sm_max_mhz"] or 1965) / 1e3
-    peak_tops = SM_COUNT * LANES_PER_CLK_PER_SM * f_ghz * 1e9 / 1e12
-    ops = OPS_PER_CELL if stats.get("packed16") else OPS_PER_CELL_32
-    achieved_tops = ops * cells_rank / (align_avg_ms / 1e3) / 1e12
-    if stats.get("packed16"):
+    kernel_gcups = cells_rank / (align_avg_ms / 1e3) / 1e9
+    packed16 = bool(stats.get("packed16"))
+    if packed16:
         tiers = [32 >> t for t in range(3) if stats.get("tier_pairs", [1, 0, 0])[t]]
         kname = " + ".join(f"align16_kernel<{k // 2}>" for k in tiers) or "align16_kernel"
+        ksub = f"align16_kernel<{tiers[0] // 2}" if tiers else "align16_kernel"
     elif stats.get("warps_per_pair", 1) > 1:
-        kname = f"align_wide_kernel<{stats['warps_per_pair']}>"
+        kname = ksub = f"align_wide_kernel<{stats['warps_per_pair']}"
+        kname += ">"
     else:
         kname = f"align_kernel<{stats['slots_per_lane']}>"
+        ksub = f"align_kernel<{stats['slots_per_lane']}"
+    # achieved = I_cell int32 lane-ops per cell x cells / kernel time;
+    # peak = P_int (measured lane-instructions/s) x 2 for the .S16x2 datapath (two int16
+    # lane-ops per lane-instruction), x 1 for the 32-bit kernels
+    lanes_per_instr = 2 if packed16 else 1
+    peak_tops = SM_COUNT * P_INT_LANES_PER_CLK_PER_SM * lanes_per_instr * f_ghz * 1e9 / 1e12
+    achieved_tops = I_CELL * kernel_gcups * 1e9 / 1e12
+    # the builder's tighter roof: the minimal ALU-pipe instruction count of this kernel's
+    # formulation, against 64 ALU lanes/clk/SM
+    ops = OPS_PER_CELL if packed16 else OPS_PER_CELL_32
+    alu_peak = SM_COUNT * LANES_PER_CLK_PER_SM * f_ghz * 1e9 / 1e12
     roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops,
-                "unit": "T ALU lane-instr/s", "frac": achieved_tops / peak_tops,
-                "traffic": TRAFFIC.get(kname), "traffic_unit": "bytes/launch (ncu dram read+write)",
-                "kernel": kname, "kernel_ms": align_avg_ms,
-                "kernel_gcups": cells_rank / (align_avg_ms / 1e3) / 1e9,
-                "gcups_roof": peak_tops * 1e12 / ops / 1e9,
-                "ops_per_cell": ops,
-                "peak_basis": f"148 SM x 64 ALU lanes/clk x {f_ghz:.3f} GHz (clocks.max.sm); "
-                              "ops_per_cell = minimal DPX .S16x2 ALU lane-instructions per cell"}
+                "unit": "T int lane-ops/s", "frac": achieved_tops / peak_tops,
+                "kernel": kname, "kernel_ms": align_avg_ms, "kernel_gcups": kernel_gcups,
+                "basis": (f"SURVEY.md §8(d): I_cell = {I_CELL} int lane-ops per cell; peak = 148 SM x "
+                          f"{P_INT_LANES_PER_CLK_PER_SM} lane-instr/clk/SM (measured, profiles/r01_dpx16.jsonl) x "
+                          f"{lanes_per_instr} ({'.S16x2: two int16 lane-ops per lane-instruction' if packed16 else 'int32'})"
+                          f" x {f_ghz:.3f} GHz (clocks.max.sm)"),
+                "gcups_roof": peak_tops * 1e12 / I_CELL / 1e9,
+                "alu_minimum": {"ops_per_cell": ops, "gcups_roof": alu_peak * 1e12 / ops / 1e9,
+                                "frac": kernel_gcups * 1e9 * ops / (alu_peak * 1e12),
+                                "basis": "minimal ALU-pipe lane-instructions per cell of this kernel's "
+                                         "formulation (DESIGN.md §6.3) vs 148 SM x 64 ALU lanes/clk"}}
+    # traffic and pipe utilisation from the newest committed ncu captures of this kernel
+    dram = newest_profile("*ncu*dram*.csv")
+    if dram:
+        m = ncu_kernel_metrics(dram, ksub)
+        if "dram__bytes_read.sum" in m:
+            roofline["traffic"] = m["dram__bytes_read.sum"] + m.get("dram__bytes_write.sum", 0.0)
+            roofline["traffic_source"] = os.path.relpath(dram, ROOT)
+            roofline["traffic_unit"] = "bytes/launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
+    if "traffic" not in roofline:
+        roofline["traffic"] = None
+    full_sum = newest_profile("*ncu*full_summary.csv")
+    if full_sum:
+        m = ncu_kernel_metrics(full_sum, ksub)
+        key = "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"
+        if key in m:
+            roofline["ncu_alu_pipe_busy_pct"] = m[key]
+            roofline["ncu_issue_active_pct"] = m.get("smsp__issue_active.avg.pct_of_peak_sustained_active")
+            roofline["ncu_source"] = os.path.relpath(full_sum, ROOT)
 
     cpu = None
     parity = None
     if not args.no_cpu:
         # the CPU baseline is timed at N = 1 only; at N > 1 rank 0 still checks a smaller
         # sample of its shard against the oracle (parity), untimed
-        stride = args.cpu_sample or max(1, n // (1000 if world == 1 else 200))
+        stride = args.cpu_sample or max(1, n_local // (1000 if world == 1 else 200))
         idx, ores, dt = run_oracle_sample(pairs, params, stride)
         if world == 1:
-            cpu = {"value": float(ores["cells"].sum()) / dt / 1e9, "unit": "GCUPS", "cores": cpu_cores(),
-                   "kind": "oracle", "sample": f"every {stride}th pair of rank 0's {n} ({len(idx)} pairs, "
-                                               f"{dt:.1f} s)"}
+            # single-core rate on a smaller sample (every 8th pair of the same sample)
+            idx1, ores1, dt1 = run_oracle_sample(pairs, params, stride * 8, threads=1)
+            cpu = dict({"value": float(ores["cells"].sum()) / dt / 1e9, "unit": "GCUPS", "cores": cpu_cores(),
+                        "kind": "oracle", "sample": f"every {stride}th pair of rank 0's {n_local} ({len(idx)} pairs, "
+                                                    f"{dt:.1f} s)",
+                        "single_core_gcups": float(ores1["cells"].sum()) / dt1 / 1e9,
+                        "single_core_sample": f"every {stride * 8}th pair ({len(idx1)} pairs, {dt1:.1f} s, 1 thread)"},
+                       **cpu_info())
         mism = int((res[idx] != ores).sum())
         parity = {"pairs_checked": int(len(idx)), "mismatches": mism}
 
+    par = (f"{world} GPU(s) claim pairs from one shared counter (system-scope atomics, NEXT #1)"
+           if dynamic else (f"LPT partition over nominal cells into {world} shards, NCCL all_gather"
+                            if world > 1 else "1 GPU"))
     line = {
         "metric": "GCUPS", "value": gcups, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": dict(config_dict(cfg, n, world), balance=args.balance,
-                       parallelism=(f"{world} GPU(s) claim pairs from one shared counter "
-                                    "(system-scope atomics, NEXT #1)") if dynamic
-                       else f"pairs sharded over {world} GPU(s)"),
+        "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "int16x2 (exact under the host guard; int32 results)" if packed16 else "int32",
+        "data": "synthetic",
+        "config": dict(config_dict(cfg, n_local, world, n_global), balance=args.balance,
+                       parallelism=par, scaling=args.scaling),
         "alignments_per_s": aln_s,
         "cells_per_step": cells_all, "zdrop_terminated": int((res["zdrop_antidiag"] >= 0).sum()),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": state["launches"],
-        "library_launches": stats["library_launches"] * args.steps,
+        "paper_speedup": PAPER_SPEEDUP,
+        "gpu_launches": launches_all,
+        "library_launches": stats["library_launches"] * args.steps * world,
         "stats_last_step": stats, "clocks": clocks, "parity": parity,
         "gen_seconds": gen_s,
     }
+    if world > 1:
+        line["rank0_pairs"] = n_local
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -96,7 +96,14 @@ typedef struct {
                      and writes only their result rows; all other rows of `out` are
                      zero-filled.  The caller resets the counter (agatha_queue_reset)
                      before the participants start and merges their outputs (each row is
-                     non-zero in exactly one, e.g. an all-reduce sum).                   */
+                     non-zero in exactly one, e.g. an all-reduce sum).
+                     Constraint: all participants must pass the same batch, params and
+                     AGATHA_ORDER_INPUT / _SINGLE_TIER / _FORCE_32BIT bits; under a queue
+                     the order ignores input chunking, so host and device inputs (and
+                     any AGATHA_CHUNK_BYTES) agree.  The first participant stores a
+                     fingerprint of these (pair count, every pair's lengths, params,
+                     flags; not the bases) in the queue; a participant whose fingerprint
+                     differs returns AGATHA_EINVAL before claiming any pair.          */
 } agatha_batch_t;
 
 /* Per-pair result: 24 bytes, written in pair order. */
@@ -164,10 +171,11 @@ int agatha_localmax_trace(agatha_ctx_t* ctx, const agatha_batch_t* batch,
                           int32_t* ref_i, int64_t cap, void* cuda_stream);
 
 /* NEXT #1: a shared pair counter for agatha_batch_t.queue.  _create allocates zeroed
- * device counters (four int32, one per slot tier) on the context's device and returns
+ * device counters (int32 [0..2], one per slot tier, and the batch fingerprint at [8];
+ * 256 bytes) on the context's device and returns
  * their CUDA IPC handle (64 bytes) for other processes; _open maps a handle from another
  * process (peer access over NVLink when on another GPU) into this context; _reset zeroes
- * the counters on `cuda_stream`;
+ * the counters and the fingerprint on `cuda_stream` (before each batch);
  * _close releases a created (opened = 0) or opened (opened = 1) counter. */
 int agatha_queue_create(agatha_ctx_t* ctx, int32_t** queue, uint8_t handle[64]);
 int agatha_queue_open(agatha_ctx_t* ctx, const uint8_t handle[64], int32_t** queue);

@@ -27,6 +27,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 
@@ -1404,6 +1405,17 @@ __global__ void pack_seq_kernel(const uint8_t* __restrict__ seq, uint64_t len, u
   if (err) atomicOr(err_flags, 1);
 }
 
+// ---- NEXT #1: shared-queue fingerprint check ------------------------------------------
+// queue[8] holds the fingerprint of the first participant of this batch (0 = none yet);
+// *err = 1 when this participant's differs.
+__global__ void queue_fp_kernel(int* queue, uint32_t fp, const unsigned long long* len_hash, int* err) {
+  const unsigned long long h = *len_hash;
+  fp ^= (uint32_t)h ^ (uint32_t)(h >> 32);
+  if (fp == 0u) fp = 1u;
+  const uint32_t old = atomicCAS_system((unsigned int*)queue + 8, 0u, fp);
+  *err = (old != 0u && old != fp) ? 1 : 0;
+}
+
 // ---- a2: validation + nominal work (one warp per pair) ------------------------------
 
 struct PrepArgs {
@@ -1427,7 +1439,16 @@ struct PrepArgs {
                                 // range): the queue reaches them after they have arrived
   int* tier_count;              // [3] pairs per slot tier (tier_of)
   int* max_off16_t0;            // max (-D) mod 16 over the pairs of tier 0
+  unsigned long long* len_hash; // shared queue (NEXT #1): sum over pairs of a hash of
+                                // (p, m, n), the batch part of the queue fingerprint
 };
+
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
 
 // Slot tier of a pair of the 16-bit kernel (DESIGN.md §6.1 "Slot tiers"): the narrowest
 // of 32 / 16 / 8 slots per lane (NREG 16 / 8 / 4) whose 32-lane front holds its D
@@ -1482,6 +1503,8 @@ __global__ void prep_kernel(PrepArgs P) {
         P.key64[p] = (tier << P.tier_shift) | (grp << 32) | (uint64_t)(0xffffffffu - nom);
       }
       P.bad[p] = (uint8_t)(flag != 0);
+      if (P.len_hash)
+        atomicAdd(P.len_hash, splitmix(splitmix(splitmix(p) ^ (unsigned long long)m) ^ (unsigned long long)n));
       if (flag) {
         atomicOr(P.err_flags, flag);
         if (P.tier_count) atomicAdd(P.tier_count, 1);  // (the call then fails anyway)
@@ -1624,7 +1647,10 @@ void score_table16(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
 
 template <int NREG, bool TRACE, int NCAP>
 int occupancy16() {  // resident blocks per SM
-  static int occ = -1;
+  // cached per instantiation; contexts on several host threads may race to fill it
+  // (they compute the same value), so the cache is an atomic
+  static std::atomic<int> cache{-1};
+  int occ = cache.load(std::memory_order_relaxed);
   if (occ < 0) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align16_kernel<NREG, TRACE, NCAP>,
                                                       32 * Front16<NREG>::wpb, 0) != cudaSuccess) {
@@ -1632,6 +1658,7 @@ int occupancy16() {  // resident blocks per SM
       occ = 1;
     }
     if (occ < 1) occ = 1;
+    cache.store(occ, std::memory_order_relaxed);
   }
   return occ;
 }
@@ -1671,13 +1698,15 @@ int launch_align16_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, in
 
 template <int W, bool TRACE>
 int launch_align_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
-  static int occ = -1;
+  static std::atomic<int> cache{-1};  // see occupancy16
+  int occ = cache.load(std::memory_order_relaxed);
   if (occ < 0) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align_wide_kernel<W, TRACE>, 32 * W, 0) != cudaSuccess) {
       cudaGetLastError();
       occ = 1;
     }
     if (occ < 1) occ = 1;
+    cache.store(occ, std::memory_order_relaxed);
   }
   const long long want = (long long)ctx->num_sms * occ;  // persistent: one pair per block
   const long long need = (long long)A.n_pairs;
@@ -1691,13 +1720,15 @@ int launch_align_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int*
 
 template <int K, bool TRACE>
 int launch_align(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
-  static int occ = -1;
+  static std::atomic<int> cache{-1};  // see occupancy16
+  int occ = cache.load(std::memory_order_relaxed);
   if (occ < 0) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align_kernel<K, TRACE>, 128, 0) != cudaSuccess) {
       cudaGetLastError();
       occ = 1;
     }
     if (occ < 1) occ = 1;
+    cache.store(occ, std::memory_order_relaxed);
   }
   const long long want = (long long)ctx->num_sms * occ;      // persistent: fill every SM once
   const long long need = ((long long)A.n_pairs + 3) / 4;    // 4 warps (pairs in flight) per block
@@ -1792,7 +1823,12 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   // longest-first group.  Estimates (conservative: a fast kernel, a slow link):
   // kernel = sum min(m,n)*D / 4 TCUPS, copy = bytes / 20 GB/s, margin 1.25.
   int lpt_from = nchunks;
-  if (!dev_in && nchunks > 2) {
+  if (b->queue) {
+    // a shared queue (NEXT #1): every participant must derive the same order, so the
+    // chunk grouping (which depends on the input memory and AGATHA_CHUNK_BYTES) is off:
+    // one longest-first group per tier
+    lpt_from = 0;
+  } else if (!dev_in && nchunks > 2) {
     const double t_kernel = est_cells / 4e12, t_copy = (double)(tot_r + tot_q) / 20e9;
     const double f = t_kernel > 0 ? 1.25 * t_copy / t_kernel : 1.0;
     if (f < 1.0) lpt_from = std::max(1, (int)std::ceil(f * nchunks));
@@ -1823,7 +1859,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   // [4..6] pairs per slot tier [7] max (-D) mod 16 of tier 0 [8] [9] queues of tiers 1, 2
   int* d_sc = (int*)ctx->scalars.p;
   int* d_ready = (int*)ctx->ready.p;
-  CUDA_TRY(cudaMemsetAsync(d_sc, 0, 40, st));
+  CUDA_TRY(cudaMemsetAsync(d_sc, 0, 64, st));
   CUDA_TRY(cudaMemcpyAsync(ctx->chunk_first.p, ctx->h_chunk_first, 8 * (nchunks + 1),
                            cudaMemcpyHostToDevice, st));
   if (dev_in) CUDA_TRY(cudaMemcpyAsync(d_ready, ctx->h_ones, 4, cudaMemcpyHostToDevice, st));
@@ -1843,6 +1879,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   while ((1 << chunk_bits) < nchunks) ++chunk_bits;
   pa.tier_shift = 32 + chunk_bits; pa.tier_count = d_sc + 4; pa.max_off16_t0 = d_sc + 7;
   pa.lpt_from = lpt_from;
+  pa.len_hash = b->queue ? (unsigned long long*)(d_sc + 12) : nullptr;  // zeroed with d_sc
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
   CUDA_TRY(cudaGetLastError());
@@ -1866,6 +1903,34 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
 
   const int K = maxD <= 512 ? 16 : 32;
   const bool k16 = use16(p, maxD) && !(b->flags & AGATHA_FORCE_32BIT);
+  if (b->queue) {
+    // Participants of a shared queue claim positions of ONE order with one counter per
+    // launch: they must agree on the batch, the parameters and every choice that shapes
+    // the order or the launches.  The fingerprint covers the pair count, every pair's
+    // (index, m, n) (hashed by the prep kernel), the parameters and the flags; not the
+    // bases themselves.  The first participant stores a fingerprint of those in
+    // the queue (queue[8]); a participant whose fingerprint differs is refused before it
+    // claims anything (agatha.h, agatha_queue_create).
+    uint32_t fp = 2166136261u;
+    auto mix = [&fp](uint64_t v) {
+      for (int i = 0; i < 8; ++i) { fp ^= (uint32_t)(v & 0xff); fp *= 16777619u; v >>= 8; }
+    };
+    mix(P); mix((uint64_t)tier_n[0]); mix((uint64_t)tier_n[1]); mix((uint64_t)tier_n[2]);
+    mix((uint64_t)maxD); mix((uint64_t)k16);
+    mix(b->flags & (AGATHA_ORDER_INPUT | AGATHA_SINGLE_TIER | AGATHA_FORCE_32BIT));
+    mix((uint64_t)(uint32_t)p->match | ((uint64_t)(uint32_t)p->mismatch << 32));
+    mix((uint64_t)(uint32_t)p->ambig | ((uint64_t)(uint32_t)p->gap_open << 32));
+    mix((uint64_t)(uint32_t)p->gap_extend | ((uint64_t)(uint32_t)p->band_left << 32));
+    mix((uint64_t)(uint32_t)p->band_right | ((uint64_t)(uint32_t)p->zdrop << 32));
+    mix((uint64_t)(uint32_t)p->variant);
+    mix(tot_r); mix(tot_q);
+    if (fp == 0) fp = 1;
+    queue_fp_kernel<<<1, 1, 0, st>>>(b->queue, fp, (const unsigned long long*)(d_sc + 12), d_sc + 15);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars + 15, d_sc + 15, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (ctx->h_scalars[15]) return AGATHA_EINVAL;
+  }
   const bool tr = trace_pair >= 0;
   // Slot tiers: each pair runs at the narrowest front that holds its
   // band, one persistent launch per non-empty tier on its own stream, so the narrow
@@ -2060,7 +2125,8 @@ int agatha_ctx_create(agatha_ctx_t** out, int device) {
   if (cudaMallocHost(&ctx->h_scalars, 64) != cudaSuccess ||
       cudaMallocHost(&ctx->h_ones, 4 * kMaxChunks) != cudaSuccess ||
       cudaMallocHost(&ctx->h_chunk_first, 8 * (kMaxChunks + 1)) != cudaSuccess) {
-    delete ctx;
+    cudaGetLastError();
+    agatha_ctx_destroy(ctx);  // releases the events, streams and any pinned buffer made
     return AGATHA_ENOMEM;
   }
   for (int i = 0; i < kMaxChunks; ++i) ctx->h_ones[i] = 1;
@@ -2098,6 +2164,7 @@ int agatha_localmax_trace(agatha_ctx_t* ctx, const agatha_batch_t* batch, const 
                           uint64_t pair, int32_t* score, int32_t* ref_i, int64_t cap, void* stream) {
   if (!ctx || !batch || !score || !ref_i || cap <= 0 || pair >= batch->n_pairs) return AGATHA_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(ctx->device));
   int rc = grow(ctx->trace, 8 * (size_t)cap + sizeof(agatha_result_t) * batch->n_pairs);
   if (rc) return rc;
   int* ts = (int*)ctx->trace.p;
@@ -2165,6 +2232,7 @@ int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* b, const agatha_params_
   pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1; pa.max_off16 = d_sc + 3;
   pa.chunk_first = nullptr; pa.nchunks = 1; pa.chunk_of = nullptr; pa.key64 = nullptr;
   pa.tier_shift = 32; pa.tier_count = nullptr; pa.max_off16_t0 = nullptr; pa.lpt_from = 1;
+  pa.len_hash = nullptr;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
   CUDA_TRY(cudaGetLastError());
@@ -2222,7 +2290,8 @@ int agatha_queue_open(agatha_ctx_t* ctx, const uint8_t handle[64], int32_t** que
 int agatha_queue_reset(agatha_ctx_t* ctx, int32_t* queue, void* stream) {
   if (!ctx || !queue) return AGATHA_EINVAL;
   CUDA_TRY(cudaSetDevice(ctx->device));
-  CUDA_TRY(cudaMemsetAsync(queue, 0, 4 * sizeof(int32_t), (cudaStream_t)stream));  // one per slot tier
+  // the tier counters [0..2] and the batch fingerprint [8]
+  CUDA_TRY(cudaMemsetAsync(queue, 0, 16 * sizeof(int32_t), (cudaStream_t)stream));
   return AGATHA_OK;
 }
 

@@ -140,11 +140,20 @@ CONFIGS["CW2"] = dataclasses.replace(CONFIGS["C2"], name="CW2", n_pairs=10_000, 
 _lib: Optional[ctypes.CDLL] = None
 
 
+# Version of the generated bytes: bump it whenever any pair of any config would change
+# (tools/oracle_cache.py keys cached oracle results on it).  Additive API changes that
+# leave every pair's bytes identical keep it.
+GENERATOR_VERSION = "splitmix64-walk-v1"
+
+
 def build(force: bool = False) -> str:
-    """Compile libagatha_synth.so in-tree with gcc (plain C, no CUDA)."""
+    """Compile libagatha_synth.so in-tree with gcc (plain C, no CUDA).  The library is
+    replaced atomically, so a process that has the old one loaded keeps running."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", _LIB, _SRC,
+        tmp = f"{_LIB}.{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC,
                                "-lm", "-lpthread"])
+        os.replace(tmp, _LIB)
     return _LIB
 
 
@@ -159,6 +168,10 @@ def _load() -> ctypes.CDLL:
         lib.synth_fill.argtypes = [ctypes.POINTER(_Cfg), ctypes.c_uint64, ctypes.c_uint64,
                                    ctypes.c_uint64, u64p, u64p, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_int]
+        lib.synth_lengths_idx.argtypes = [ctypes.POINTER(_Cfg), ctypes.c_uint64, u64p,
+                                          ctypes.c_uint64, u64p, u64p]
+        lib.synth_fill_idx.argtypes = [ctypes.POINTER(_Cfg), ctypes.c_uint64, u64p, ctypes.c_uint64,
+                                       u64p, u64p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -216,6 +229,37 @@ def generate(cfg: Config, k0: int = 0, k1: Optional[int] = None, threads: Option
     nt = threads or min(64, os.cpu_count() or 1)
     _load().synth_fill(ctypes.byref(c), cfg.seed, k0, k1, _p64(roff), _p64(qoff),
                        ctypes.c_void_p(R.ctypes.data), ctypes.c_void_p(Q.ctypes.data), nt)
+    return Pairs(R, roff, Q, qoff)
+
+
+def lengths_idx(cfg: Config, idx):
+    """(ref, query) lengths of pairs idx[0..] of cfg's stream."""
+    idx = np.ascontiguousarray(idx, np.uint64)
+    rl = np.zeros(len(idx), np.uint64)
+    ql = np.zeros(len(idx), np.uint64)
+    c = cfg._c()
+    _load().synth_lengths_idx(ctypes.byref(c), cfg.seed, _p64(idx), len(idx), _p64(rl), _p64(ql))
+    return rl, ql
+
+
+def generate_idx(cfg: Config, idx, threads: Optional[int] = None, pinned_out=None) -> Pairs:
+    """Generate pairs idx[0], idx[1], ... of ``cfg`` (any subset, in that order): position t
+    holds exactly the bytes ``generate`` gives pair idx[t]."""
+    idx = np.ascontiguousarray(idx, np.uint64)
+    rl, ql = lengths_idx(cfg, idx)
+    roff = np.zeros(len(rl) + 1, np.uint64)
+    qoff = np.zeros(len(ql) + 1, np.uint64)
+    np.cumsum(rl, out=roff[1:])
+    np.cumsum(ql, out=qoff[1:])
+    if pinned_out is not None:
+        R, Q = pinned_out(int(roff[-1]), int(qoff[-1]))
+    else:
+        R = np.empty(int(roff[-1]), np.uint8)
+        Q = np.empty(int(qoff[-1]), np.uint8)
+    c = cfg._c()
+    nt = threads or min(64, os.cpu_count() or 1)
+    _load().synth_fill_idx(ctypes.byref(c), cfg.seed, _p64(idx), len(idx), _p64(roff), _p64(qoff),
+                           ctypes.c_void_p(R.ctypes.data), ctypes.c_void_p(Q.ctypes.data), nt)
     return Pairs(R, roff, Q, qoff)
 
 

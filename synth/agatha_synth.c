@@ -145,6 +145,7 @@ typedef struct {
   uint8_t *R, *Q;
   volatile uint64_t* next;
   pthread_mutex_t* mu;
+  const uint64_t* idx; /* NULL: pairs k0..k1-1; else pairs idx[0..k1-k0-1] */
 } fill_job_t;
 
 static void* fill_worker(void* arg) {
@@ -159,7 +160,7 @@ static void* fill_worker(void* arg) {
     uint64_t kend = k + 64 < j->k1 ? k + 64 : j->k1;
     for (; k < kend; ++k) {
       const uint64_t t = k - j->k0;
-      fill_one(j->c, j->seed, k, j->R + j->roff[t], j->Q + j->qoff[t]);
+      fill_one(j->c, j->seed, j->idx ? j->idx[t] : k, j->R + j->roff[t], j->Q + j->qoff[t]);
     }
   }
   return NULL;
@@ -175,7 +176,38 @@ int synth_fill(const synth_cfg_t* c, uint64_t seed, uint64_t k0, uint64_t k1, co
   volatile uint64_t next = k0;
   pthread_mutex_t mu;
   pthread_mutex_init(&mu, NULL);
-  fill_job_t job = {c, seed, k0, k1, roff, qoff, R, Q, &next, &mu};
+  fill_job_t job = {c, seed, k0, k1, roff, qoff, R, Q, &next, &mu, NULL};
+  pthread_t th[256];
+  for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, fill_worker, &job);
+  fill_worker(&job);
+  for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+  pthread_mutex_destroy(&mu);
+  return 0;
+}
+
+/* The same pairs by index: pair idx[t] of the stream at position t (a rank's share of a
+ * partition that is not a contiguous range, bench.py --gpus N).  Identical bytes to
+ * synth_lengths / synth_fill for every pair. */
+int synth_lengths_idx(const synth_cfg_t* c, uint64_t seed, const uint64_t* idx, uint64_t n,
+                      uint64_t* rlen, uint64_t* qlen) {
+  if (!c) return -1;
+  for (uint64_t t = 0; t < n; ++t) {
+    const uint64_t Ls = draw_len(c, seed, idx[t]);
+    qlen[t] = Ls;
+    rlen[t] = ref_len_of(c, Ls);
+  }
+  return 0;
+}
+
+int synth_fill_idx(const synth_cfg_t* c, uint64_t seed, const uint64_t* idx, uint64_t n,
+                   const uint64_t* roff, const uint64_t* qoff, uint8_t* R, uint8_t* Q, int nthreads) {
+  if (!c) return -1;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  volatile uint64_t next = 0;
+  pthread_mutex_t mu;
+  pthread_mutex_init(&mu, NULL);
+  fill_job_t job = {c, seed, 0, n, roff, qoff, R, Q, &next, &mu, idx};
   pthread_t th[256];
   for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, fill_worker, &job);
   fill_worker(&job);

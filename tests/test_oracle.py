@@ -300,3 +300,47 @@ def test_variants_vs_bruteforce_random():
         p["variant"] = int(rng.integers(0, 8))
         rc, got = oracle.align_one(R, Q, p)
         assert tuple(got) == tuple(bruteforce.align(R, Q, **p)), (R, Q, p)
+
+
+# oracle_align_batch (the batch driver every GPU parity test checks against) is pinned
+# row by row: it slices pairs by the offsets, reorders them longest first over its worker
+# threads and scatters each record back to out[k].  A slicing, ordering or scatter
+# mistake would put some pair's record in another pair's row, so every row must equal
+# both the single-pair oracle and the brute-force path enumeration of THAT pair.
+def test_align_batch_rows_equal_align_one_and_bruteforce():
+    rng = np.random.default_rng(2024)
+    for trial in range(6):
+        pairs_l = []
+        for _ in range(70):
+            m, n = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+            R = "".join(rng.choice(list("ACGTN"), m, p=[0.24, 0.24, 0.24, 0.24, 0.04]))
+            Q = "".join(rng.choice(list("ACGTN"), n, p=[0.24, 0.24, 0.24, 0.24, 0.04]))
+            if rng.random() < 0.4:
+                Q = R[:n]
+            pairs_l.append((R, Q))
+        # unequal lengths in shuffled order: the longest-first reorder permutes the rows
+        lens = [len(r) + len(q) for r, q in pairs_l]
+        assert sorted(lens, reverse=True) != lens
+        p = _rand_params(rng)
+        batch = synth.from_list(pairs_l)
+        for threads in (1, 3, 8):
+            rc, res, status = oracle.align_batch(batch, p, threads=threads)
+            assert rc == 0 and not status.any()
+            for k, (R, Q) in enumerate(pairs_l):
+                rc1, one = oracle.align_one(R, Q, p)
+                assert rc1 == 0
+                assert tuple(res[k].tolist()) == tuple(one), (trial, threads, k)
+                if threads == 1:
+                    assert tuple(res[k].tolist()) == tuple(bruteforce.align(R, Q, **p)), (trial, k)
+
+
+def test_align_batch_rows_equal_align_one_on_c1_slice():
+    cfg = synth.CONFIGS["C1"]
+    pairs = synth.generate(cfg, 0, 48)
+    params = vars(cfg.scoring)
+    rc, res, _ = oracle.align_batch(pairs, params, threads=4)
+    assert rc == 0
+    assert len(set(res["cells"].tolist())) > 40  # rows are distinguishable
+    for k in range(pairs.n_pairs):
+        R, Q = pairs.pair(k)
+        assert tuple(res[k].tolist()) == tuple(oracle.align_one(R, Q, params)[1]), k

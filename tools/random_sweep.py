@@ -71,6 +71,21 @@ def params(rng):
                 band_right=br, zdrop=z, variant=var)
 
 
+def exceeds_limits(lst, prm) -> bool:
+    """True when at least one pair is outside the GPU's documented range:
+    clipped band D > 4096, or alpha + max(bl,br)*beta + max(a,b,n)*min(m,n) >= 2^20 - 16."""
+    mx = max(prm["match"], prm["mismatch"], prm.get("ambig", prm["mismatch"]))
+    for R, Q in lst:
+        m, n = len(R), len(Q)
+        bl = n if prm["band_left"] < 0 or prm["band_left"] > n else prm["band_left"]
+        br = m if prm["band_right"] < 0 or prm["band_right"] > m else prm["band_right"]
+        if bl + br + 1 > 4096:
+            return True
+        if prm["gap_open"] + max(bl, br) * prm["gap_extend"] + mx * min(m, n) >= (1 << 20) - 16:
+            return True
+    return False
+
+
 def main():
     from paper_2403_06478_b200 import agatha
     nb = int(sys.argv[1]) if len(sys.argv) > 1 else 40
@@ -97,7 +112,9 @@ def main():
                 "rc_oracle": rc, "packed16": st.get("packed16"), "tier_pairs": st.get("tier_pairs")}
         if got is None:
             # the GPU may refuse what the oracle accepts only for its documented limits
-            line["ok"] = rc_gpu == agatha.ERANGE
+            # (DESIGN.md §7): some pair must really exceed D <= 4096 or the |H| bound
+            line["ok"] = rc_gpu == agatha.ERANGE and exceeds_limits(lst, prm)
+            line["limit_checked"] = True
         else:
             bad = np.nonzero(got != exp)[0]
             line["mismatches"] = int(len(bad))

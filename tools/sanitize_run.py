@@ -1,5 +1,5 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck): both kernels,
-all three slot tiers (the edge corpus at w = 500 needs all of them), streamed host inputs
+the wide-band tier (D > 1024), a two-context shared queue, all three slot tiers (the edge corpus at w = 500 needs all of them), streamed host inputs
 in many chunks, the trace path, pack4 and plan on C1 pairs plus an edge corpus."""
 import os
 import sys
@@ -25,6 +25,29 @@ for p in (pairs, edge):
                     dict(vars(cfg.scoring), band_left=0, band_right=3),
                     dict(vars(cfg.scoring), band_left=0, band_right=0)):
             agatha.align_pairs(ctx, p, prm, flags=flags)
+# wide-band tier (D > 1024: two and four warps per pair, align_wide_kernel)
+wide = synth.generate(synth.CONFIGS["CW1"], 0, 3)
+wide = synth.from_list([(R[:3000], Q[:3000]) for R, Q in (wide.pair(k) for k in range(3))])
+for prm in (dict(vars(cfg.scoring), band_left=700, band_right=700, zdrop=400),
+            dict(vars(cfg.scoring), band_left=1500, band_right=1600, zdrop=-1)):
+    agatha.align_pairs(ctx, wide, prm)
+# a shared queue (NEXT #1, system-scope claims) drained by two contexts on two threads
+import threading  # noqa: E402
+ls = synth.generate(synth.CONFIGS["LS10"], 0, 96)
+ctx2 = agatha.Context(0)
+q = agatha.SharedQueue.create(ctx)
+q.reset()
+torch.cuda.synchronize()
+outs = [np.zeros(ls.n_pairs, agatha.RESULT_DTYPE) for _ in range(2)]
+th = [threading.Thread(target=agatha.align_pairs_q, args=(c, ls, vars(synth.CONFIGS["LS10"].scoring), outs[k], q))
+      for k, c in enumerate((ctx, ctx2))]
+for t in th:
+    t.start()
+for t in th:
+    t.join()
+assert int(((outs[0]["cells"] != 0) | (outs[1]["cells"] != 0)).sum()) == ls.n_pairs
+q.close()
+ctx2.close()
 R, Q = pairs.pair(3)
 agatha.localmax_trace(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, vars(cfg.scoring), 3,
                       len(R) + len(Q) + 1)
