@@ -86,6 +86,9 @@ def parse():
     ap.add_argument("--tiers", default="split", choices=["split", "single"],
                     help="16-bit kernel: each pair at its own slot tier (default) or one "
                          "launch at the widest front (ablation; input order implies single)")
+    ap.add_argument("--refill", default="queue", choices=["queue", "static"],
+                    help="queue: persistent warps refill from the work queue (default); "
+                         "static: warp u takes order positions u, u+W, ... (no-refill ablation)")
     ap.add_argument("--balance", default="static", choices=["static", "dynamic"],
                     help="static: fixed per-rank shards; dynamic: every rank holds the whole "
                          "batch and the persistent kernels claim pairs from one counter in "
@@ -376,6 +379,8 @@ def main():
     flags = agatha.ORDER_INPUT if args.order == "input" else 0
     if args.tiers == "single":
         flags |= agatha.SINGLE_TIER
+    if args.refill == "static":
+        flags |= agatha.STATIC_ASSIGN
     ctx = agatha.Context(local)
     stream = torch.cuda.current_stream()
     queue = None
@@ -596,7 +601,8 @@ def main():
         "dtype": "int16x2 (exact under the host guard; int32 results)" if packed16 else "int32",
         "data": "synthetic",
         "config": dict(config_dict(cfg, n_local, world, n_global), balance=args.balance,
-                       parallelism=par, scaling=args.scaling),
+                       parallelism=par, scaling=args.scaling, order=args.order, tiers=args.tiers,
+                       refill=args.refill),
         "alignments_per_s": aln_s,
         "cells_per_step": cells_all, "zdrop_terminated": int((res["zdrop_antidiag"] >= 0).sum()),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

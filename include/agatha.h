@@ -56,6 +56,11 @@ extern "C" {
                                      batch's widest band needs, in one launch, instead of
                                      each pair at the narrowest slot tier that holds its
                                      band (tier ablation; results are identical)          */
+#define AGATHA_STATIC_ASSIGN 128u /* no work queue: persistent warp u of a launch takes the
+                                     order positions u, u + W, u + 2W, ... (W warps), so a
+                                     warp that finishes early is not refilled (the analogue
+                                     of the paper's no-rejoining baseline, P:754-761;
+                                     results are identical; not with a shared queue)      */
 
 /* Scoring (Eq. 1-4 symbols).  Penalties are POSITIVE numbers. */
 typedef struct {

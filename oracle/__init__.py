@@ -81,8 +81,10 @@ _lib: Optional[ctypes.CDLL] = None
 def build(force: bool = False) -> str:
     """Compile the oracle (plain C, gcc -O2).  Building the checker is not using it."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", _LIB, _SRC,
+        tmp = f"{_LIB}.{os.getpid()}.tmp"  # replaced atomically: a running user keeps the old one
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC,
                                "-lpthread"])
+        os.replace(tmp, _LIB)
     return _LIB
 
 

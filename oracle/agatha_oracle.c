@@ -185,9 +185,14 @@ int oracle_align_one(const uint8_t* R, int64_t m, const uint8_t* Q, int64_t n,
 
   /* step 4: c = 2, 3, ..., m+n */
   for (int64_t c = 2; c <= m + n; ++c) {
-    /* 4a: cells(c) = {(i, c-i) : max(1,c-n) <= i <= min(m,c-1), -bl <= 2i-c <= br} */
+    /* 4a: cells(c) = {(i, c-i) : max(1,c-n) <= i <= min(m,c-1), -bl <= 2i-c <= br}: the
+     * table range of i intersected with the band range ceil((c-bl)/2) <= i <=
+     * floor((c+br)/2) (the in_band test below stays as a literal filter) */
     int64_t ilo = c - n > 1 ? c - n : 1;
     int64_t ihi = c - 1 < m ? c - 1 : m;
+    const int64_t blo = (c - s.bl + 1) >> 1, bhi = (c + s.br) >> 1;
+    if (blo > ilo) ilo = blo;
+    if (bhi < ihi) ihi = bhi;
     int any = 0;
     int32_t L_H = 0;
     int64_t L_i = 0;

@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_PKG, "libagatha.so")
 OK, EINVAL, EEMPTY, ECHAR, ERANGE, ECUDA, ENOMEM = 0, -1, -2, -3, -4, -5, -6
 MEM_HOST, MEM_DEVICE, OUT_DEVICE = 0, 1, 2
 N_REJECT, N_MAP, PACK_REVERSE, ORDER_INPUT, FORCE_32BIT, SINGLE_TIER = 0, 4, 8, 16, 32, 64
+STATIC_ASSIGN = 128  # ablation: no work queue, warp u takes order positions u, u + W, ...
 
 RESULT_DTYPE = np.dtype([("score", "<i4"), ("ref_end", "<i4"), ("query_end", "<i4"),
                          ("zdrop_antidiag", "<i4"), ("cells", "<i8")])

@@ -71,6 +71,7 @@ struct AlignArgs {
   agatha_result_t* out;
   int* queue;                // global work counter (a7)
   int sysq;                  // 1: the counter is shared across GPUs/processes (system scope)
+  int static_assign;         // 1: no queue, unit u takes positions u + k * nunits (ablation)
   uint32_t n_pairs;
   int bl, br;                // band; negative = unbounded
   int alpha, beta, zdrop;
@@ -88,9 +89,13 @@ struct AlignArgs {
                              // a re-centring (negative)
 };
 
-// a7: the next position of the dispatch order.  A shared counter (NEXT #1) lives in
-// another GPU's or process's memory, so it is claimed with a system-scope atomic.
-__device__ __forceinline__ int claim_next(const AlignArgs& A) {
+// a7: the next position of the dispatch order for work unit `unit` of `nunits` (a warp,
+// or a block of the wide tier), whose k-th claim this is.  A shared counter (NEXT #1) lives
+// in another GPU's or process's memory, so it is claimed with a system-scope atomic.  The
+// static ablation (AGATHA_STATIC_ASSIGN, the analogue of the paper's no-refill baseline,
+// P:754-761) gives unit u the positions u, u + nunits, u + 2 nunits, ... with no queue.
+__device__ __forceinline__ int claim_next(const AlignArgs& A, int unit, int nunits, int& k) {
+  if (A.static_assign) return unit + (k++) * nunits;
   return A.sysq ? atomicAdd_system(A.queue, 1) : atomicAdd(A.queue, 1);
 }
 
@@ -482,9 +487,11 @@ struct MinBlocks { static constexpr int value = K >= 32 ? 3 : 4; };
 template <int K, bool TRACE>
 __global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignArgs A) {
   const int lane = threadIdx.x & 31;
+  const int unit = blockIdx.x * 4 + (threadIdx.x >> 5), nunits = gridDim.x * 4;
+  int k = 0;
   for (;;) {
     int q = 0;
-    if (lane == 0) q = claim_next(A);
+    if (lane == 0) q = claim_next(A, unit, nunits, k);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
     align_pair<K, TRACE>(A, A.order[q], lane);
@@ -743,8 +750,9 @@ template <int W, bool TRACE>
 __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A) {
   __shared__ WideShared sh;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int k = 0;
   for (;;) {
-    if (threadIdx.x == 0) sh.q = claim_next(A);
+    if (threadIdx.x == 0) sh.q = claim_next(A, blockIdx.x, gridDim.x, k);
     __syncthreads();
     const int q = sh.q;
     __syncthreads();  // every thread has read q before thread 0 takes the next one
@@ -799,10 +807,33 @@ __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A)
 #ifndef AGATHA_VOTE_NARROW
 #define AGATHA_VOTE_NARROW 0  // the same for the 16- and 8-slot fronts: no vote (+0.3-2.3%)
 #endif
-constexpr int kW16 = -29250;       // "-infinity" (walls, E/F of boundary cells)
-constexpr int kCapNeg16 = -21250;  // padding cap
-constexpr int kEmpty16 = -17250;   // lane max at or below: no valid cell on the anti-diagonal
-constexpr int kTop16 = -129;       // every stored H is at most this
+// Issue-slot trims of the steady loop (A/B switches):
+//   LMTREE   the 32-slot front's lane max over its eight registers as a depth-2 tree
+//   SNAP128  the deferred-argmax snapshot as 128-bit shared stores
+//   STEADYC  the steady phase keeps the previous anti-diagonal's cell range and base
+//            instead of re-setting them every step (re-centring adjusts rH_prev)
+#ifndef AGATHA_LMTREE
+#define AGATHA_LMTREE 1
+#endif
+#ifndef AGATHA_SNAP128
+#define AGATHA_SNAP128 0
+#endif
+#ifndef AGATHA_STEADYC
+#define AGATHA_STEADYC 1
+#endif
+// Stored half-words live in [kW16, kTop16 + 127].  With AGATHA_POS16 (default) the domain
+// is shifted up by kShift16 into [2495, 31743]: every live half-word is then a positive
+// int16 whose bit pattern is also a finite, normal, positive fp16, and positive fp16 bit
+// patterns order exactly like the integers, so pure min/max steps may run as fp16x2
+// HMNMX2; the IMAD diagonal add stays carry-free (low half + 127 <= 31743).
+#ifndef AGATHA_POS16
+#define AGATHA_POS16 1
+#endif
+constexpr int kShift16 = AGATHA_POS16 ? 31745 : 0;
+constexpr int kW16 = -29250 + kShift16;       // "-infinity" (walls, E/F of boundary cells)
+constexpr int kCapNeg16 = -21250 + kShift16;  // padding cap
+constexpr int kEmpty16 = -17250 + kShift16;   // lane max at or below: no valid cell on the anti-diagonal
+constexpr int kTop16 = -129 + kShift16;       // every stored H is at most this
 #ifndef AGATHA_REBASE16
 #define AGATHA_REBASE16 32
 #endif
@@ -834,10 +865,25 @@ __device__ __forceinline__ uint32_t shr16_fma(uint32_t x, uint32_t k65536) {
   asm("mad.hi.s32 %0, %1, %2, 0;" : "=r"(d) : "r"((int)x), "r"((int)k65536));
   return d;
 }
-__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vmins2(a, b); }
+[[maybe_unused]] __device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vmins2(a, b); }
+// Pure max / min of two half-word pairs as fp16x2 HMNMX2 (AGATHA_POS16 domain: every
+// operand that matters is a positive int16 <= 31743 = 0x7BFF, i.e. a finite positive fp16
+// whose order is the integer order; exact on all pairs in [0, 0x7BFF],
+// profiles/r02_hmnmx.jsonl).  It issues on the ALU pipe (same file), so AGATHA_HMAX is off.
+[[maybe_unused]] __device__ __forceinline__ uint32_t hmax2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+[[maybe_unused]] __device__ __forceinline__ uint32_t hmin2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
 // Half-word pair add h + s on the FMA pipe (IMAD h * one + s).  Exact with no carry
-// between the halves because every stored H half is in [-32768, kTop16] and every
-// s half in [0, 127]: each low-half sum stays negative, so it never wraps past 0xFFFF.
+// between the halves because every stored H half is in [kW16, kTop16] and every s half in
+// [0, 127]: a low-half sum stays below 0xFFFF (negative halves, AGATHA_POS16 = 0) or
+// below 0x7BFF (positive halves, AGATHA_POS16 = 1), so it never carries.
 __device__ __forceinline__ uint32_t add16x2_fma(uint32_t h, uint32_t s, uint32_t one) {
   uint32_t d;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(h), "r"(one), "r"(s));
@@ -883,12 +929,35 @@ __device__ __forceinline__ int argmax_diag16(int first, int P, int dlo) {
   return dlo + ls * (2 * NREG) + slot;
 }
 
+// Word of the deferred-argmax snapshot holding register k (of one parity) of `lane`.
+template <int NREG>
+__device__ __forceinline__ int snap_word(int k, int lane) {
+  if (AGATHA_SNAP128 && NREG >= 8) return (k >> 2) * 128 + lane * 4 + (k & 3);
+  if (AGATHA_SNAP128 && NREG == 4) return lane * 2 + k;
+  return k * 32 + lane;
+}
+
+template <int NREG, int PARC>
+__device__ __forceinline__ void store_snapshot(uint32_t* snap, const uint32_t (&H)[NREG], int lane) {
+  if (AGATHA_SNAP128 && NREG >= 8) {
+#pragma unroll
+    for (int q = 0; q < NREG / 8; ++q)
+      reinterpret_cast<uint4*>(snap)[q * 32 + lane] =
+          make_uint4(H[PARC + 8 * q], H[PARC + 8 * q + 2], H[PARC + 8 * q + 4], H[PARC + 8 * q + 6]);
+  } else if (AGATHA_SNAP128 && NREG == 4) {
+    reinterpret_cast<uint2*>(snap)[lane] = make_uint2(H[PARC], H[PARC + 2]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < NREG / 2; ++k) snap[k * 32 + lane] = H[PARC + 2 * k];
+  }
+}
+
 template <int NREG>
 __device__ __forceinline__ void resolve_G16(State16& s, const uint32_t* snap, int lane) {
   if (s.posValid) return;
   uint32_t r[NREG / 2];
 #pragma unroll
-  for (int k = 0; k < NREG / 2; ++k) r[k] = snap[k * 32 + lane];
+  for (int k = 0; k < NREG / 2; ++k) r[k] = snap[snap_word<NREG>(k, lane)];
   const int v = s.G_H + s.alpha * s.G_c - s.snapB;
   const int d = argmax_diag16<NREG>(first_slot16<NREG>(r, v, s.snapTlo, s.snapThi), s.snapPar, s.dlo);
   s.G_d = d;
@@ -944,8 +1013,7 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
   }
   if (upd) {
     // defer the argmax: keep the anti-diagonal's registers (one per lane) in shared memory
-#pragma unroll
-    for (int k = 0; k < NREG / 2; ++k) snap[k * 32 + lane] = H[PARC + 2 * k];
+    store_snapshot<NREG, PARC>(snap, H, lane);
     s.snapB = s.B;
     s.snapPar = PARC;
     s.snapTlo = tlo;
@@ -971,6 +1039,27 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
 // kCapNeg16.  Its high end is NREG-aligned, so the wall there is a half-word of the
 // PAR = 1 exchange (KEEPX clears it to -inf in the one lane that needs it), and the slots
 // above it are never read by a band cell; LMK removes them from the lane max.
+// Pure min/max steps as fp16x2 HMNMX2 (AGATHA_POS16 only): bit 0 the padding caps, bit 1
+// the lane max of the two halves.  Measured: HMNMX2 issues on the ALU pipe like
+// VIMNMX.S16x2 (profiles/r02_hmnmx.jsonl), and with both bits ptxas allots 164 registers
+// and C2 falls 3592 -> 3400 GCUPS, so the default is 0.
+#ifndef AGATHA_HMAX
+#define AGATHA_HMAX 0
+#endif
+#ifndef AGATHA_PIN_CONSTS
+#define AGATHA_PIN_CONSTS 0
+#endif
+#if AGATHA_POS16 && (AGATHA_HMAX & 1)
+#define HCAP(a, b) hmin2(a, b)
+#else
+#define HCAP(a, b) vmin2(a, b)
+#endif
+#if AGATHA_POS16 && (AGATHA_HMAX & 2)
+#define HLMAX(a, b) hmax2(a, b)
+#else
+#define HLMAX(a, b) vmax2(a, b)
+#endif
+
 template <int NREG, int NCAP, int PAR, bool MASKED>
 __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], uint32_t (&F)[NREG],
                                       const uint32_t (&CAP)[NCAP], const uint32_t (&S2)[NREG / 2],
@@ -991,6 +1080,7 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
     xEF = (prmt(F[0], sf, 0x5432) & KEEPX) | (W2 & ~KEEPX);
   }
   uint32_t lm = W2, prev = W2;
+  uint32_t hv[NREG / 2];
 #pragma unroll
   for (int k = 0; k < NREG / 2; ++k) {
     const int j = PAR + 2 * k;
@@ -1005,7 +1095,7 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
 #else
     uint32_t h = vaddmax2(H[j], S2[k], vmax2(e, f));                    // Eq. 1 (shifted)
 #endif
-    if (j < NCAP) h = vmin2(h, CAP[j < NCAP ? j : 0]);         // padding slots stay <= kCapNeg16
+    if (j < NCAP) h = HCAP(h, CAP[j < NCAP ? j : 0]);          // padding slots stay <= kCapNeg16
     H[j] = h;
     E[j] = e;
     F[j] = f;
@@ -1014,7 +1104,15 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
       const uint32_t M = ((V2 >> k) & 0x00010001u) * 0xFFFFu;
       h = (h & M) | (W2 & ~M);
     }
-    if (k & 1) lm = __vimax3_s16x2(lm, prev, h); else prev = h;  // Eq. 5, per half
+    if (AGATHA_LMTREE && NREG == 16) {
+      hv[k] = h;
+    } else {
+      if (k & 1) lm = __vimax3_s16x2(lm, prev, h); else prev = h;  // Eq. 5, per half
+    }
+  }
+  if (AGATHA_LMTREE && NREG == 16) {  // depth 2: max3(max3(h0..h2), max3(h3..h5), max(h6, h7))
+    lm = __vimax3_s16x2(__vimax3_s16x2(hv[0], hv[1], hv[2]), __vimax3_s16x2(hv[3], hv[4], hv[5]),
+                        vmax2(hv[6], hv[7 % (NREG / 2)]));
   }
   if ((NREG / 2) & 1) lm = vmax2(lm, prev);
   lm = (lm & LMK) | (W2 & ~LMK);  // slots above the band's high wall
@@ -1023,9 +1121,10 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
   // an int32 is exactly max(lo, hi)
 #if AGATHA_LMSHL
   // (lm << 16 as a full-rate IMAD): the high half becomes max(hi, lo) and the low half
-  // max(lo, 0) = 0, so the lane value is max(lo, hi) * 65536 and the warp max is
-  // recovered by one uniform shift after the REDUX (LANEMAX16)
-  return (int)vmax2(lm, lm * k65536);
+  // max(lo, 0) (= 0 for negative halves, lo for AGATHA_POS16), so the high half of the
+  // lane value is max(lo, hi) and the warp max is recovered by one uniform arithmetic
+  // shift after the REDUX (LANEMAX16); the low half only breaks ties between lanes
+  return (int)HLMAX(lm, lm * k65536);
 #else
   return (int)vmax2(lm, (uint32_t)hi16_fma(lm, k65536));
 #endif
@@ -1113,7 +1212,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     for (int h = 0; h < 2; ++h) {
       const int k = j + h * NREG, g = K * lane + k, d = dls + g;
       const bool valid = g >= off && g < gend;
-      c2[h] = valid ? 32767 : kCapNeg16;
+      c2[h] = valid ? kTop16 + 127 : kCapNeg16;  // no cap: the largest live value
       const int ci = ((k & 1) == 0) ? cb - 2 : cb - 1;  // (dls + K*lane) has parity of cb
       v2[h] = valid ? (d == 0 ? 0 : bnd(d) + alpha * ci) - s.B : kCapNeg16;
     }
@@ -1144,7 +1243,17 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   };
   prefetch();
 
+#if AGATHA_PIN_CONSTS
+  // pinned in vector registers: a volatile copy cannot be rematerialised, so ptxas keeps
+  // the table words instead of re-copying them from uniform registers before every lookup
+  uint32_t T0, T1, k65536, one;
+  asm volatile("mov.b32 %0, %1;" : "=r"(T0) : "r"(A.T16_0));
+  asm volatile("mov.b32 %0, %1;" : "=r"(T1) : "r"(A.T16_1));
+  asm volatile("mov.b32 %0, %1;" : "=r"(k65536) : "r"(A.k65536));
+  asm volatile("mov.b32 %0, %1;" : "=r"(one) : "r"(A.one));
+#else
   const uint32_t T0 = A.T16_0, T1 = A.T16_1, k65536 = A.k65536, one = A.one;
+#endif
   const int ref16 = -s.B;
   int rH_prev = kEmpty16 - 1, B_prev = s.B, tlo_prev = 0, thi_prev = NC - 1;
   bool stop = false;
@@ -1230,9 +1339,11 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
-      B_prev = s.B;
-      tlo_prev = MASKED ? tlo : 0;
-      thi_prev = MASKED ? thi : NC - 1;
+      if (!AGATHA_STEADYC || MASKED) {
+        B_prev = s.B;
+        tlo_prev = MASKED ? tlo : 0;
+        thi_prev = MASKED ? thi : NC - 1;
+      }
     }
     // ---- step PAR = 1, anti-diagonal cb + 1 ----
     {
@@ -1258,9 +1369,11 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
-      B_prev = s.B;
-      tlo_prev = MASKED ? tlo : 0;
-      thi_prev = MASKED ? thi : NC - 1;
+      if (!AGATHA_STEADYC || MASKED) {
+        B_prev = s.B;
+        tlo_prev = MASKED ? tlo : 0;
+        thi_prev = MASKED ? thi : NC - 1;
+      }
     }
     cb += 2;
     ++u;
@@ -1288,6 +1401,10 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       // one-diagonal band, where every other one is empty, runs the 32-bit kernel)
       if (rH_prev > kEmpty16) {
         const int delta = rH_prev + B_prev - s.B - ref16;
+        if (AGATHA_STEADYC) {  // the steady steps do not refresh B_prev: keep rH_prev in s.B units
+          rH_prev -= delta - (B_prev - s.B);
+          B_prev = s.B + delta;
+        }
         const uint32_t nd2 = pack2(-delta, -delta);
 #pragma unroll
         for (int j = 0; j < NREG; ++j) {
@@ -1384,9 +1501,11 @@ __global__ void __launch_bounds__(32 * Front16<NREG>::wpb, Front16<NREG>::minb) 
   __shared__ uint32_t snap_all[Front16<NREG>::wpb][NREG / 2 * 32];
   __shared__ uint32_t pref_all[Front16<NREG>::wpb][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int unit = blockIdx.x * Front16<NREG>::wpb + warp, nunits = gridDim.x * Front16<NREG>::wpb;
+  int k = 0;
   for (;;) {
     int q = 0;
-    if (lane == 0) q = claim_next(A);
+    if (lane == 0) q = claim_next(A, unit, nunits, k);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
     align_pair16<NREG, TRACE, NCAP>(A, A.order[q], lane, snap_all[warp], pref_all[warp]);
@@ -1749,6 +1868,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   if (rc) return rc;
   if (b->n_pairs == 0) return AGATHA_EEMPTY;
   if (b->n_pairs >= (1ull << 31)) return AGATHA_ERANGE;
+  if (b->queue && (b->flags & AGATHA_STATIC_ASSIGN)) return AGATHA_EINVAL;  // no queue to share
   CUDA_TRY(cudaSetDevice(ctx->device));
   memset(&ctx->stats, 0, sizeof(ctx->stats));
   const uint64_t P = b->n_pairs;
@@ -1966,6 +2086,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   A.out = d_out; A.n_pairs = (uint32_t)P;
   A.queue = b->queue ? b->queue : d_sc + 2;  // NEXT #1: a counter shared with other GPUs
   A.sysq = b->queue ? 1 : 0;
+  A.static_assign = (b->flags & AGATHA_STATIC_ASSIGN) ? 1 : 0;
   if (b->queue)  // rows this participant does not claim stay zero (merged by the caller)
     CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(agatha_result_t) * P, st));
   A.bl = p->band_left; A.br = p->band_right;

@@ -201,6 +201,12 @@ def test_slot_tiers_mixed_batch(gpu_lib, ctx):
     assert one.tobytes() == got.tobytes()
     inp = gpu_lib.align_pairs(ctx, pairs, params, flags=gpu_lib.ORDER_INPUT)
     assert inp.tobytes() == got.tobytes()
+    # the no-refill ablation (static warp assignment) in both orders, and with the 32-bit
+    # kernel, gives the same bytes
+    for fl in (gpu_lib.STATIC_ASSIGN, gpu_lib.STATIC_ASSIGN | gpu_lib.ORDER_INPUT,
+               gpu_lib.STATIC_ASSIGN | gpu_lib.FORCE_32BIT):
+        st_ = gpu_lib.align_pairs(ctx, pairs, params, flags=fl)
+        assert st_.tobytes() == got.tobytes(), fl
     # a batch that is all narrow runs the NREG = 4 front alone
     short = pairs.subset([k for k in range(len(lst)) if k % 3 == 0])
     compare(gpu_lib, ctx, short, params)
