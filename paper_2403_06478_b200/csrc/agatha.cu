@@ -821,6 +821,17 @@ __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A)
 #ifndef AGATHA_STEADYC
 #define AGATHA_STEADYC 1
 #endif
+//   SNAPSLIM the snapshot stores only the registers, the base and G: the parity and cell
+//            range of the snapshot's anti-diagonal are recomputed from G_c when resolved,
+//            validity is G_c == posC, and a disabled Z-drop uses a huge threshold
+//   LOOPSLIM the iteration carries one window offset (oQ = 7 - oR) and no u (masked
+//            steps derive it from cb)
+#ifndef AGATHA_SNAPSLIM
+#define AGATHA_SNAPSLIM 1
+#endif
+#ifndef AGATHA_LOOPSLIM
+#define AGATHA_LOOPSLIM 0
+#endif
 // Stored half-words live in [kW16, kTop16 + 127].  With AGATHA_POS16 (default) the domain
 // is shifted up by kShift16 into [2495, 31743]: every live half-word is then a positive
 // int16 whose bit pattern is also a finite, normal, positive fp16, and positive fp16 bit
@@ -900,6 +911,8 @@ struct State16 {
   int zthr;                   // G_H - Z (INT_MIN when Z is off or there is no G yet)
   bool posValid;
   int snapB, snapPar, snapTlo, snapThi;
+  int posC;                   // SNAPSLIM: G_i, G_j, G_d hold the position of G at anti-diagonal posC
+  int zeff;                   // SNAPSLIM: Z, or 2^30 when Z-drop is off
   int term;
 };
 
@@ -954,12 +967,29 @@ __device__ __forceinline__ void store_snapshot(uint32_t* snap, const uint32_t (&
 
 template <int NREG>
 __device__ __forceinline__ void resolve_G16(State16& s, const uint32_t* snap, int lane) {
-  if (s.posValid) return;
+  int par, tlo, thi;
+  if (AGATHA_SNAPSLIM) {
+    if (s.posC == s.G_c) return;
+    // the snapshot's anti-diagonal c = G_c: register parity and in-table cell range of this
+    // lane, as the masked steps compute them (step PAR = 0 holds c = 2u - dlo)
+    const int c = s.G_c;
+    par = (c - s.dlo) & 1;
+    const int u = (c - par + s.dlo) >> 1;
+    const int ib = u + par + lane * NREG, jb = u - s.dlo - lane * NREG;
+    tlo = max(1 - ib, jb - s.n);
+    thi = min(s.m - ib, jb - 1);
+    s.posC = c;
+  } else {
+    if (s.posValid) return;
+    par = s.snapPar;
+    tlo = s.snapTlo;
+    thi = s.snapThi;
+  }
   uint32_t r[NREG / 2];
 #pragma unroll
   for (int k = 0; k < NREG / 2; ++k) r[k] = snap[snap_word<NREG>(k, lane)];
   const int v = s.G_H + s.alpha * s.G_c - s.snapB;
-  const int d = argmax_diag16<NREG>(first_slot16<NREG>(r, v, s.snapTlo, s.snapThi), s.snapPar, s.dlo);
+  const int d = argmax_diag16<NREG>(first_slot16<NREG>(r, v, tlo, thi), par, s.dlo);
   s.G_d = d;
   s.G_i = (s.G_c + d) >> 1;
   s.G_j = s.G_c - s.G_i;
@@ -1015,13 +1045,17 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
     // defer the argmax: keep the anti-diagonal's registers (one per lane) in shared memory
     store_snapshot<NREG, PARC>(snap, H, lane);
     s.snapB = s.B;
-    s.snapPar = PARC;
-    s.snapTlo = tlo;
-    s.snapThi = thi;
     s.G_H = Hs;
     s.G_c = c;
-    s.zthr = s.zdrop >= 0 ? Hs - s.zdrop : INT_MIN;
-    s.posValid = false;
+    if (AGATHA_SNAPSLIM) {
+      s.zthr = Hs - s.zeff;
+    } else {
+      s.snapPar = PARC;
+      s.snapTlo = tlo;
+      s.snapThi = thi;
+      s.zthr = s.zdrop >= 0 ? Hs - s.zdrop : INT_MIN;
+      s.posValid = false;
+    }
   }
   return false;
 }
@@ -1176,6 +1210,8 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     s.zthr = A.zdrop >= 0 ? -A.zdrop : INT_MIN;
   }
   s.snapB = 0; s.snapPar = 0; s.snapTlo = 0; s.snapThi = 0; s.term = -1;
+  s.posC = 0;  // = G_c: the initial position (none, or the origin) is resolved
+  s.zeff = A.zdrop >= 0 ? A.zdrop : (1 << 30);
   const int dlo = -bl, D = Dband;
   const uint32_t AmB2 = pack2(alpha - beta, alpha - beta);
   const int gend = off + D;  // first slot above the band (a multiple of NREG)
@@ -1311,8 +1347,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   auto iteration = [&](auto masked_tag) {
     constexpr bool MASKED = decltype(masked_tag)::value;
     uint32_t qg[2], S2[NREG / 2], V2 = 0u, rs[2];
-    qg[0] = __funnelshift_rc(Wq0, Wq1, 4 * oQ);
-    qg[1] = __funnelshift_rc(Wq1, Wq2, 4 * oQ);
+    const int oq4 = AGATHA_LOOPSLIM ? 28 - 4 * oR : 4 * oQ;
+    qg[0] = __funnelshift_rc(Wq0, Wq1, oq4);
+    qg[1] = __funnelshift_rc(Wq1, Wq2, oq4);
 #if AGATHA_S2EARLY
     // both steps' scores up front: the PAR = 1 lookups (with their long-latency IMAD.HI)
     // then issue under the PAR = 0 cells instead of stalling in front of PAR = 1
@@ -1330,7 +1367,8 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
       int tlo = 0, thi = NC;
       if (MASKED) {
-        const int ib = u + lane * NC, jb = u - dls - lane * NC;
+        const int uu = AGATHA_LOOPSLIM ? (cb + dls) >> 1 : u;
+        const int ib = uu + lane * NC, jb = uu - dls - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
         V2 = valid_bits(tlo, thi);
@@ -1360,7 +1398,8 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
       int tlo = 0, thi = NC;
       if (MASKED) {
-        const int ib = u + 1 + lane * NC, jb = u - dls - lane * NC;
+        const int uu = AGATHA_LOOPSLIM ? (cb + dls) >> 1 : u;
+        const int ib = uu + 1 + lane * NC, jb = uu - dls - lane * NC;
         tlo = max(1 - ib, jb - n);
         thi = min(m - ib, jb - 1);
         V2 = valid_bits(tlo, thi);
@@ -1376,9 +1415,11 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
     }
     cb += 2;
-    ++u;
+    if (!AGATHA_LOOPSLIM) {
+      ++u;
+      --oQ;
+    }
     ++oR;
-    --oQ;
   };
 
   // Window refills (every 8 iterations for each sequence) and base re-centring happen
@@ -1496,8 +1537,15 @@ template <int NREG> struct Front16 {
   static constexpr int minb = NREG >= 16 ? AGATHA_MINB16 : (NREG >= 8 ? AGATHA_MINB8 : AGATHA_MINB4);
 };
 
+// The 32-slot front may instead be built with an exact register cap (__maxnreg__) and no
+// minimum-blocks bound, to run more warps per SM at the register count ptxas chose for
+// 12 (A/B switch: AGATHA_MAXNREG16 = the cap, with AGATHA_WPB16 / AGATHA_MINB16 giving
+// the block shape and the blocks per SM the launch assumes).
+#ifndef AGATHA_MAXNREG16
+#define AGATHA_MAXNREG16 0
+#endif
 template <int NREG, bool TRACE, int NCAP>
-__global__ void __launch_bounds__(32 * Front16<NREG>::wpb, Front16<NREG>::minb) align16_kernel(AlignArgs A) {
+__device__ __forceinline__ void align16_body(const AlignArgs& A) {
   __shared__ uint32_t snap_all[Front16<NREG>::wpb][NREG / 2 * 32];
   __shared__ uint32_t pref_all[Front16<NREG>::wpb][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1511,6 +1559,18 @@ __global__ void __launch_bounds__(32 * Front16<NREG>::wpb, Front16<NREG>::minb) 
     align_pair16<NREG, TRACE, NCAP>(A, A.order[q], lane, snap_all[warp], pref_all[warp]);
   }
 }
+
+template <int NREG, bool TRACE, int NCAP>
+__global__ void __launch_bounds__(32 * Front16<NREG>::wpb, Front16<NREG>::minb) align16_kernel(AlignArgs A) {
+  align16_body<NREG, TRACE, NCAP>(A);
+}
+
+#if AGATHA_MAXNREG16
+template <int NREG, bool TRACE, int NCAP>
+__global__ void __maxnreg__(AGATHA_MAXNREG16) align16w_kernel(AlignArgs A) {
+  align16_body<NREG, TRACE, NCAP>(A);
+}
+#endif
 
 // ---- a1: pack (one warp per pair; R forward, Q reversed) ---------------------------
 
@@ -1771,8 +1831,12 @@ int occupancy16() {  // resident blocks per SM
   static std::atomic<int> cache{-1};
   int occ = cache.load(std::memory_order_relaxed);
   if (occ < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, align16_kernel<NREG, TRACE, NCAP>,
-                                                      32 * Front16<NREG>::wpb, 0) != cudaSuccess) {
+#if AGATHA_MAXNREG16
+    const auto kfn = NREG == 16 ? align16w_kernel<NREG, TRACE, NCAP> : align16_kernel<NREG, TRACE, NCAP>;
+#else
+    const auto kfn = align16_kernel<NREG, TRACE, NCAP>;
+#endif
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 32 * Front16<NREG>::wpb, 0) != cudaSuccess) {
       cudaGetLastError();
       occ = 1;
     }
@@ -1798,6 +1862,10 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
   int grid = (int)(want < need ? want : need);
   if (grid < 1) grid = 1;
   *grid_out = grid;
+#if AGATHA_MAXNREG16
+  if (NREG == 16) align16w_kernel<NREG, TRACE, NCAP><<<grid, 32 * wpb, 0, st>>>(A);
+  else
+#endif
   align16_kernel<NREG, TRACE, NCAP><<<grid, 32 * wpb, 0, st>>>(A);
   CUDA_TRY(cudaGetLastError());
   return AGATHA_OK;
