@@ -187,6 +187,33 @@ int agatha_queue_open(agatha_ctx_t* ctx, const uint8_t handle[64], int32_t** que
 int agatha_queue_reset(agatha_ctx_t* ctx, int32_t* queue, void* cuda_stream);
 int agatha_queue_close(agatha_ctx_t* ctx, int32_t* queue, int opened);
 
+/* NEXT #1: a FEDERATED batch for cross-GPU dynamic
+ * balancing without replicated inputs.  The global batch is the concatenation, in owner
+ * order, of n_owners (1..8) device batches: owners[o] holds owner o's ASCII sequences and
+ * offsets (flags must include AGATHA_MEM_DEVICE; pointers may be peer-mapped memory of
+ * another GPU or process, from agatha_ipc_open, read over NVLink).  Global pair g of
+ * owner o is its local pair g - (pairs of owners 0..o-1).  Every participant passes the
+ * same owners (its own mapping of them), params and `flags` (AGATHA_ORDER_INPUT,
+ * _SINGLE_TIER, _FORCE_32BIT, _N_MAP), and the same `queue` (agatha_queue_*): the
+ * persistent kernels claim global pairs from the one order, read a claimed pair's
+ * inputs from its owner, and write its 24-byte record to row g of `out` (a DEVICE
+ * buffer of 24 * total pairs, owned by the caller); rows the participant did not claim
+ * are zero (merge as for agatha_batch_t.queue).  queue = NULL: this context aligns the
+ * whole global batch.  The result of every pair equals agatha_align_batch's on the
+ * concatenated batch.  Errors as agatha_align_batch; EINVAL also for a host-memory
+ * owner or n_owners outside 1..8, ERANGE for 2^31 or more pairs in total. */
+int agatha_align_federated(agatha_ctx_t* ctx, const agatha_batch_t* owners, int n_owners,
+                           const agatha_params_t* params, agatha_result_t* out, int32_t* queue,
+                           uint32_t flags, void* cuda_stream);
+
+/* Device buffers shareable across processes (CUDA IPC): _alloc returns `bytes` of device
+ * memory on the context's device and its 64-byte IPC handle; _open maps another
+ * process's handle into this context (peer access over NVLink when on another GPU);
+ * _close frees an allocated (opened = 0) or unmaps an opened (opened = 1) buffer. */
+int agatha_ipc_alloc(agatha_ctx_t* ctx, uint64_t bytes, void** ptr, uint8_t handle[64]);
+int agatha_ipc_open(agatha_ctx_t* ctx, const uint8_t handle[64], void** ptr);
+int agatha_ipc_close(agatha_ctx_t* ctx, void* ptr, int opened);
+
 int agatha_get_stats(const agatha_ctx_t* ctx, agatha_stats_t* stats);
 const char* agatha_strerror(int code);
 int agatha_version(void);

@@ -86,6 +86,11 @@ def _load() -> ctypes.CDLL:
     lib.agatha_queue_open.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(vp)]
     lib.agatha_queue_reset.argtypes = [vp, vp, vp]
     lib.agatha_queue_close.argtypes = [vp, vp, ctypes.c_int]
+    lib.agatha_align_federated.argtypes = [vp, ctypes.POINTER(Batch), ctypes.c_int, ctypes.POINTER(Params),
+                                           vp, vp, ctypes.c_uint32, vp]
+    lib.agatha_ipc_alloc.argtypes = [vp, u64, ctypes.POINTER(vp), ctypes.c_char_p]
+    lib.agatha_ipc_open.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(vp)]
+    lib.agatha_ipc_close.argtypes = [vp, vp, ctypes.c_int]
     return lib
 
 
@@ -95,7 +100,8 @@ _lib = _load()
 EXPORTS = ("agatha_ctx_create", "agatha_ctx_destroy", "agatha_align_batch", "agatha_pack4",
            "agatha_plan", "agatha_localmax_trace", "agatha_get_stats", "agatha_strerror",
            "agatha_version", "agatha_queue_create", "agatha_queue_open", "agatha_queue_reset",
-           "agatha_queue_close")
+           "agatha_queue_close", "agatha_align_federated", "agatha_ipc_alloc", "agatha_ipc_open",
+           "agatha_ipc_close")
 
 
 def lib() -> ctypes.CDLL:
@@ -209,6 +215,84 @@ class SharedQueue:
         if self.ptr:
             _lib.agatha_queue_close(self.ctx.handle, self.ptr, int(self.opened))
             self.ptr = 0
+
+
+class IpcBuffer:
+    """Device memory another process can map (agatha_ipc_*): ``IpcBuffer.alloc(ctx, n)``
+    allocates n bytes and exposes ``handle`` (64 bytes); ``IpcBuffer.open(ctx, handle, n)``
+    maps another process's buffer.  ``ptr`` is the device address in this process."""
+
+    def __init__(self, ctx: Context, ptr: int, nbytes: int, handle: bytes, opened: bool):
+        self.ctx, self.ptr, self.nbytes, self.handle, self.opened = ctx, ptr, nbytes, handle, opened
+
+    @classmethod
+    def alloc(cls, ctx: Context, nbytes: int) -> "IpcBuffer":
+        q = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(64)
+        rc = _lib.agatha_ipc_alloc(ctx.handle, max(int(nbytes), 1), ctypes.byref(q), h)
+        if rc != OK:
+            raise AgathaError(rc, "agatha_ipc_alloc")
+        return cls(ctx, int(q.value), int(nbytes), h.raw, False)
+
+    @classmethod
+    def open(cls, ctx: Context, handle: bytes, nbytes: int) -> "IpcBuffer":
+        q = ctypes.c_void_p()
+        rc = _lib.agatha_ipc_open(ctx.handle, bytes(handle), ctypes.byref(q))
+        if rc != OK:
+            raise AgathaError(rc, "agatha_ipc_open")
+        return cls(ctx, int(q.value), int(nbytes), bytes(handle), True)
+
+    def copy_from_host(self, arr, offset: int = 0, stream=None):
+        """Host -> this buffer (cudaMemcpyAsync on ``stream``, plumbing only)."""
+        from cuda.bindings import runtime as rt
+
+        a = np.ascontiguousarray(arr)
+        if a.nbytes + offset > self.nbytes:
+            raise ValueError("copy exceeds the buffer")
+        st = _stream_ptr(stream) or 0
+        err, = rt.cudaMemcpyAsync(self.ptr + offset, a.ctypes.data, a.nbytes,
+                                  rt.cudaMemcpyKind.cudaMemcpyHostToDevice, st)
+        if err != rt.cudaError_t.cudaSuccess:
+            raise AgathaError(ECUDA, f"cudaMemcpyAsync: {err}")
+        if stream is None:
+            rt.cudaStreamSynchronize(0)
+
+    def close(self):
+        if self.ptr:
+            _lib.agatha_ipc_close(self.ctx.handle, self.ptr, int(self.opened))
+            self.ptr = 0
+
+
+class DevicePtr:
+    """A raw device address (e.g. inside an IpcBuffer) usable where align_batch /
+    align_federated take a device array."""
+
+    is_cuda = True
+
+    def __init__(self, ptr: int, n: int):
+        self.ptr, self.n = int(ptr), int(n)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def __len__(self) -> int:
+        return self.n
+
+
+def align_federated(ctx: Context, owners, params, out, queue: Optional["SharedQueue"] = None,
+                    flags: int = 0, stream=None):
+    """agatha_align_federated.  ``owners``: list of (ref, ref_off, qry, qry_off) device
+    arrays (torch CUDA tensors or DevicePtr), one per owner, in global order; ``out``: a
+    CUDA uint8 tensor of 24 * total pairs."""
+    arr = (Batch * len(owners))()
+    for o, (ref, ref_off, qry, qry_off) in enumerate(owners):
+        arr[o] = make_batch(ref, ref_off, qry, qry_off)
+    p = params_from(params)
+    rc = _lib.agatha_align_federated(ctx.handle, arr, len(owners), ctypes.byref(p), _ptr(out),
+                                     queue.ptr if queue is not None else None, flags, _stream_ptr(stream))
+    if rc != OK:
+        raise AgathaError(rc, "agatha_align_federated")
+    return out
 
 
 def _ptr(a) -> int:

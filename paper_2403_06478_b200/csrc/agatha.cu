@@ -54,10 +54,52 @@ constexpr int kRampChunks = 5;                  // the first chunks start at 1/3
 #define AGATHA_CHUNK_RAMP 1
 #endif
 
+// A federated batch (NEXT #1, agatha_align_federated): the global batch is the
+// concatenation of up to kMaxOwners owners' device batches, each possibly in another
+// GPU's or process's memory (peer-mapped); global pair g lies in owner o with
+// start[o] <= g < start[o + 1], at local index g - start[o].  n_owners == 0: one batch.
+constexpr int kMaxOwners = 8;
+struct Owners {
+  int n_owners;
+  const uint8_t* ref[kMaxOwners];
+  const uint8_t* qry[kMaxOwners];
+  const uint64_t* roff[kMaxOwners];
+  const uint64_t* qoff[kMaxOwners];
+  uint32_t start[kMaxOwners + 1];
+};
+
+// Sequence offsets (and the owner's ASCII) of global pair p.
+struct PairSrc {
+  const uint8_t* ref;
+  const uint8_t* qry;
+  uint64_t r0, q0;
+  int64_t m, n;
+};
+__device__ __forceinline__ PairSrc pair_src(const Owners& O, const uint8_t* ref, const uint8_t* qry,
+                                            const uint64_t* roff, const uint64_t* qoff, uint64_t p) {
+  uint64_t l = p;
+  if (O.n_owners > 0) {
+    int o = 0;
+    while (o + 1 < O.n_owners && p >= O.start[o + 1]) ++o;
+    l = p - O.start[o];
+    ref = O.ref[o]; qry = O.qry[o]; roff = O.roff[o]; qoff = O.qoff[o];
+  }
+  PairSrc s;
+  s.ref = ref; s.qry = qry;
+  s.r0 = roff[l]; s.q0 = qoff[l];
+  s.m = (int64_t)(roff[l + 1] - s.r0);
+  s.n = (int64_t)(qoff[l + 1] - s.q0);
+  return s;
+}
+
 struct AlignArgs {
-  uint32_t* rw;              // packed R words, pair p's region starts at word (ref_off[p] >> 3) + 4p
-                             // (guard word, data, guard word: see load_word_rw)
-  uint32_t* qw;              // packed reversed-Q words, same addressing with qry_off
+  uint32_t* rw;              // packed R scratch: work unit u (a warp, or a wide-tier block) packs
+                             // its current pair at rw + (unit_base + u) * rstride (guard word,
+                             // data, guard word: see load_word_rw)
+  uint32_t* qw;              // packed reversed-Q scratch, qstride words per unit
+  uint64_t rstride, qstride; // words per unit: max over the batch of len / 8 + 4, rounded up
+  int unit_base;             // first scratch unit of this launch (tier launches run together)
+  Owners own;                // federated batch, or n_owners = 0
   const uint8_t* ref_ascii;  // ASCII inputs (device), packed by the align kernel (a1)
   const uint8_t* qry_ascii;
   const uint8_t* chunk_of;   // input chunk of each pair
@@ -315,10 +357,11 @@ __device__ __forceinline__ int step_cells(int (&H)[K], int (&Eh)[K], int (&Fh)[K
 }
 
 template <int K, bool TRACE>
-__device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
-  const uint64_t r0 = A.roff[pid], q0 = A.qoff[pid];
-  const int m = (int)(A.roff[pid + 1] - r0);
-  const int n = (int)(A.qoff[pid + 1] - q0);
+__device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane, int unit) {
+  const PairSrc ps = pair_src(A.own, A.ref_ascii, A.qry_ascii, A.roff, A.qoff, pid);
+  const uint64_t r0 = ps.r0, q0 = ps.q0;
+  const int m = (int)ps.m;
+  const int n = (int)ps.n;
   if (A.bad[pid]) {
     if (lane == 0) {
       agatha_result_t z = {0, 0, 0, -1, 0};
@@ -326,10 +369,10 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane) {
     }
     return;
   }
-  uint32_t* Rw = A.rw + (r0 >> 3) + 4 * pid;
-  uint32_t* Qw = A.qw + (q0 >> 3) + 4 * pid;
+  uint32_t* Rw = A.rw + (uint64_t)(A.unit_base + unit) * A.rstride;
+  uint32_t* Qw = A.qw + (uint64_t)(A.unit_base + unit) * A.qstride;
   const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
-  pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
+  pack_pair_fused(ps.ref, ps.qry, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
                   A.nmap != 0, A.err_flags, lane);
   const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;   // diagonals beyond hold no cell
   const int br = (A.br < 0 || A.br > m) ? m : A.br;
@@ -494,7 +537,7 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignAr
     if (lane == 0) q = claim_next(A, unit, nunits, k);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
-    align_pair<K, TRACE>(A, A.order[q], lane);
+    align_pair<K, TRACE>(A, A.order[q], lane, unit);
   }
 }
 
@@ -554,9 +597,10 @@ template <int W, bool TRACE>
 __device__ void align_pair_wide(const AlignArgs& A, uint32_t pid, int lane, int wid, WideShared& sh) {
   constexpr int K = 32;
   const int gl = wid * 32 + lane;
-  const uint64_t r0 = A.roff[pid], q0 = A.qoff[pid];
-  const int m = (int)(A.roff[pid + 1] - r0);
-  const int n = (int)(A.qoff[pid + 1] - q0);
+  const PairSrc ps = pair_src(A.own, A.ref_ascii, A.qry_ascii, A.roff, A.qoff, pid);
+  const uint64_t r0 = ps.r0, q0 = ps.q0;
+  const int m = (int)ps.m;
+  const int n = (int)ps.n;
   if (A.bad[pid]) {  // block-uniform
     if (gl == 0) {
       agatha_result_t z = {0, 0, 0, -1, 0};
@@ -564,10 +608,10 @@ __device__ void align_pair_wide(const AlignArgs& A, uint32_t pid, int lane, int 
     }
     return;
   }
-  uint32_t* Rw = A.rw + (r0 >> 3) + 4 * pid;
-  uint32_t* Qw = A.qw + (q0 >> 3) + 4 * pid;
+  uint32_t* Rw = A.rw + (uint64_t)(A.unit_base + (int)blockIdx.x) * A.rstride;  // one pair per block
+  uint32_t* Qw = A.qw + (uint64_t)(A.unit_base + (int)blockIdx.x) * A.qstride;
   const int nwR = (m + 7) >> 3, nwQ = (n + 7) >> 3;
-  pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
+  pack_pair_fused(ps.ref, ps.qry, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
                   A.nmap != 0, A.err_flags, gl, 0, 0, 32 * W);
   const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;
   const int br = (A.br < 0 || A.br > m) ? m : A.br;
@@ -1165,12 +1209,14 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
 }
 
 template <int NREG, bool TRACE, int NCAP>
-__device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap, uint32_t* pref) {
+__device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap, uint32_t* pref,
+                             int unit) {
   constexpr int K = 2 * NREG;        // slots per lane
   constexpr int NC = NREG;           // cells per step per lane (K/2)
-  const uint64_t r0 = A.roff[pid], q0 = A.qoff[pid];
-  const int m = (int)(A.roff[pid + 1] - r0);
-  const int n = (int)(A.qoff[pid + 1] - q0);
+  const PairSrc ps = pair_src(A.own, A.ref_ascii, A.qry_ascii, A.roff, A.qoff, pid);
+  const uint64_t r0 = ps.r0, q0 = ps.q0;
+  const int m = (int)ps.m;
+  const int n = (int)ps.n;
   if (A.bad[pid]) {
     if (lane == 0) {
       agatha_result_t z = {0, 0, 0, -1, 0};
@@ -1194,10 +1240,10 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   const int u0 = ((dls & 1) + dls) >> 1;  // u of the first step (cb = dls mod 2, below)
   const int padR = (1 - u0) & 7;
   const int padQ = (7 - (n + dls - u0)) & 7;
-  uint32_t* Rw = A.rw + (r0 >> 3) + 4 * pid;
-  uint32_t* Qw = A.qw + (q0 >> 3) + 4 * pid;
+  uint32_t* Rw = A.rw + (uint64_t)(A.unit_base + unit) * A.rstride;
+  uint32_t* Qw = A.qw + (uint64_t)(A.unit_base + unit) * A.qstride;
   const int nwR = (m + padR + 7) >> 3, nwQ = (n + padQ + 7) >> 3;
-  pack_pair_fused(A.ref_ascii, A.qry_ascii, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
+  pack_pair_fused(ps.ref, ps.qry, r0, q0, m, n, Rw, Qw, A.ready, A.chunk_of[pid],
                   A.nmap != 0, A.err_flags, lane, padR, padQ);
 
   State16 s;
@@ -1556,7 +1602,7 @@ __device__ __forceinline__ void align16_body(const AlignArgs& A) {
     if (lane == 0) q = claim_next(A, unit, nunits, k);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
-    align_pair16<NREG, TRACE, NCAP>(A, A.order[q], lane, snap_all[warp], pref_all[warp]);
+    align_pair16<NREG, TRACE, NCAP>(A, A.order[q], lane, snap_all[warp], pref_all[warp], unit);
   }
 }
 
@@ -1600,6 +1646,8 @@ __global__ void queue_fp_kernel(int* queue, uint32_t fp, const unsigned long lon
 struct PrepArgs {
   const uint64_t* roff;
   const uint64_t* qoff;
+  Owners own;       // federated batch, or n_owners = 0
+  int* max_len;     // [2] max m, max n over the batch (the packing scratch per unit), or null
   uint64_t n_pairs;
   int bl, br, alpha, beta, maxs;  // maxs = max(a, b, n)
   uint32_t* nominal;
@@ -1644,8 +1692,9 @@ __global__ void prep_kernel(PrepArgs P) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t p = warp; p < P.n_pairs; p += nwarps) {
-    const int64_t m = (int64_t)(P.roff[p + 1] - P.roff[p]);
-    const int64_t n = (int64_t)(P.qoff[p + 1] - P.qoff[p]);
+    const PairSrc ps = pair_src(P.own, nullptr, nullptr, P.roff, P.qoff, p);
+    const int64_t m = ps.m;
+    const int64_t n = ps.n;
     int flag = 0;
     int64_t bl = (P.bl < 0 || P.bl > n) ? n : P.bl;
     int64_t br = (P.br < 0 || P.br > m) ? m : P.br;
@@ -1688,6 +1737,10 @@ __global__ void prep_kernel(PrepArgs P) {
         atomicOr(P.err_flags, flag);
         if (P.tier_count) atomicAdd(P.tier_count, 1);  // (the call then fails anyway)
       } else {
+        if (P.max_len) {
+          atomicMax(P.max_len, (int)m);
+          atomicMax(P.max_len + 1, (int)n);
+        }
         atomicMax(P.max_slots, (int)D);
         atomicMax(P.max_off16, (int)((-D) & 15));
         if (P.tier_count) {
@@ -1853,8 +1906,11 @@ long long warp_slots16(const agatha_ctx* ctx, int t) {
   return (long long)ctx->num_sms * occ;
 }
 
+// Launch helpers: grid = the persistent grid; *units_out = packing-scratch units the
+// launch uses (warps, or blocks of the wide tier).  dry: size only, launch nothing.
 template <int NREG, bool TRACE, int NCAP>
-int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
+int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int* units_out = nullptr,
+                   bool dry = false) {
   const int occ = occupancy16<NREG, TRACE, NCAP>();
   const long long want = (long long)ctx->num_sms * occ;
   constexpr int wpb = Front16<NREG>::wpb;
@@ -1862,6 +1918,8 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
   int grid = (int)(want < need ? want : need);
   if (grid < 1) grid = 1;
   *grid_out = grid;
+  if (units_out) *units_out = grid * wpb;
+  if (dry) return AGATHA_OK;
 #if AGATHA_MAXNREG16
   if (NREG == 16) align16w_kernel<NREG, TRACE, NCAP><<<grid, 32 * wpb, 0, st>>>(A);
   else
@@ -1875,16 +1933,18 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
 #ifndef AGATHA_NCAP7
 #define AGATHA_NCAP7 0  // 1: seven capped registers when every off <= 7 (-0.1%)
 #endif
-int launch_align16_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int maxoff) {
+int launch_align16_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int maxoff,
+                        int* units_out = nullptr, bool dry = false) {
 #if AGATHA_NCAP7
-  if (maxoff <= 7) return launch_align16<16, false, 7>(ctx, A, st, grid_out);
+  if (maxoff <= 7) return launch_align16<16, false, 7>(ctx, A, st, grid_out, units_out, dry);
 #endif
-  if (maxoff <= 8) return launch_align16<16, false, 8>(ctx, A, st, grid_out);
-  return launch_align16<16, false, 16>(ctx, A, st, grid_out);
+  if (maxoff <= 8) return launch_align16<16, false, 8>(ctx, A, st, grid_out, units_out, dry);
+  return launch_align16<16, false, 16>(ctx, A, st, grid_out, units_out, dry);
 }
 
 template <int W, bool TRACE>
-int launch_align_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
+int launch_align_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int* units_out = nullptr,
+                      bool dry = false) {
   static std::atomic<int> cache{-1};  // see occupancy16
   int occ = cache.load(std::memory_order_relaxed);
   if (occ < 0) {
@@ -1900,13 +1960,16 @@ int launch_align_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int*
   int grid = (int)(want < need ? want : need);
   if (grid < 1) grid = 1;
   *grid_out = grid;
+  if (units_out) *units_out = grid;
+  if (dry) return AGATHA_OK;
   align_wide_kernel<W, TRACE><<<grid, 32 * W, 0, st>>>(A);
   CUDA_TRY(cudaGetLastError());
   return AGATHA_OK;
 }
 
 template <int K, bool TRACE>
-int launch_align(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out) {
+int launch_align(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int* units_out = nullptr,
+                 bool dry = false) {
   static std::atomic<int> cache{-1};  // see occupancy16
   int occ = cache.load(std::memory_order_relaxed);
   if (occ < 0) {
@@ -1922,6 +1985,8 @@ int launch_align(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid
   int grid = (int)(want < need ? want : need);
   if (grid < 1) grid = 1;
   *grid_out = grid;
+  if (units_out) *units_out = grid * 4;
+  if (dry) return AGATHA_OK;
   align_kernel<K, TRACE><<<grid, 128, 0, st>>>(A);
   CUDA_TRY(cudaGetLastError());
   return AGATHA_OK;
@@ -1930,8 +1995,9 @@ int launch_align(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid
 // Shared body of agatha_align_batch / agatha_localmax_trace.
 int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p,
               agatha_result_t* out, cudaStream_t st, long long trace_pair, int* trace_score,
-              int* trace_i, long long trace_cap) {
+              int* trace_i, long long trace_cap, const Owners* fed = nullptr) {
   if (!ctx || !b || !out) return AGATHA_EINVAL;
+  if (fed && !(b->flags & AGATHA_MEM_DEVICE)) return AGATHA_EINVAL;
   int rc = check_params(p);
   if (rc) return rc;
   if (b->n_pairs == 0) return AGATHA_EEMPTY;
@@ -1954,10 +2020,14 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   int nchunks = 1;
   double est_cells = 0.0;  // host inputs: sum of min(m,n) * D, the kernel-time estimate
   ctx->h_chunk_first[0] = 0;
-  // pinned mirror: ints [0..9] the scalars below, u64 [5] [6] the device inputs' total
+  // pinned mirror: ints [0..17] the scalars below, u64 [12] [13] the device inputs' total
   // lengths (read with the plan's scalars: one host round trip), int [14] the final flags
-  uint64_t* h_tot = (uint64_t*)ctx->h_scalars + 5;
-  if (dev_in) {
+  uint64_t* h_tot = (uint64_t*)ctx->h_scalars + 12;  // ints 24..27
+  if (fed) {  // federated: every owner's inputs are device-resident (maybe peer-mapped)
+    h_tot[0] = h_tot[1] = 0;
+    tot_r = tot_q = 0;
+    d_ref = d_qry = nullptr; d_roff = d_qoff = nullptr;
+  } else if (dev_in) {
     CUDA_TRY(cudaMemcpyAsync(h_tot, b->ref_off + P, 8, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(h_tot + 1, b->qry_off + P, 8, cudaMemcpyDeviceToHost, st));
     tot_r = tot_q = 0;  // known after the plan's synchronisation
@@ -2033,7 +2103,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   if (sort_bytes64 > sort_bytes) sort_bytes = sort_bytes64;
   if ((rc = grow(ctx->nominal, 4 * P)) || (rc = grow(ctx->nominal_sorted, 4 * P)) ||
       (rc = grow(ctx->iota, 4 * P)) || (rc = grow(ctx->order, 4 * P)) || (rc = grow(ctx->bad, P)) ||
-      (rc = grow(ctx->sort_tmp, sort_bytes)) || (rc = grow(ctx->scalars, 64)) ||
+      (rc = grow(ctx->sort_tmp, sort_bytes)) || (rc = grow(ctx->scalars, 128)) ||
       (rc = grow(ctx->chunk_first, 8 * (kMaxChunks + 1))) || (rc = grow(ctx->chunk_of, P)) ||
       (rc = grow(ctx->key64, 8 * P)) || (rc = grow(ctx->key64_sorted, 8 * P)) ||
       (rc = grow(ctx->ready, 4 * kMaxChunks)))
@@ -2045,9 +2115,10 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   }
   // scalars: [0] err_flags [1] max_slots [2] queue (tier 0 / one launch) [3] max (-D) mod 16
   // [4..6] pairs per slot tier [7] max (-D) mod 16 of tier 0 [8] [9] queues of tiers 1, 2
+  // [12..13] len_hash (shared queue) [15] fingerprint mismatch [16] [17] max m, max n
   int* d_sc = (int*)ctx->scalars.p;
   int* d_ready = (int*)ctx->ready.p;
-  CUDA_TRY(cudaMemsetAsync(d_sc, 0, 64, st));
+  CUDA_TRY(cudaMemsetAsync(d_sc, 0, 128, st));
   CUDA_TRY(cudaMemcpyAsync(ctx->chunk_first.p, ctx->h_chunk_first, 8 * (nchunks + 1),
                            cudaMemcpyHostToDevice, st));
   if (dev_in) CUDA_TRY(cudaMemcpyAsync(d_ready, ctx->h_ones, 4, cudaMemcpyHostToDevice, st));
@@ -2057,6 +2128,8 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
                                           : (p->mismatch > p->ambig ? p->mismatch : p->ambig);
   PrepArgs pa;
   pa.roff = d_roff; pa.qoff = d_qoff; pa.n_pairs = P;
+  if (fed) pa.own = *fed; else pa.own.n_owners = 0;
+  pa.max_len = d_sc + 16;
   pa.bl = p->band_left; pa.br = p->band_right; pa.alpha = p->gap_open; pa.beta = p->gap_extend;
   pa.maxs = maxs;
   pa.nominal = (uint32_t*)ctx->nominal.p; pa.iota = (uint32_t*)ctx->iota.p;
@@ -2074,18 +2147,19 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   int launches = 1, lib_launches = 0;
   const uint32_t* d_order = (const uint32_t*)ctx->iota.p;
   // K (slots per lane) from the widest band in the batch
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 40, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 72, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   const int err0 = ctx->h_scalars[0], maxD = ctx->h_scalars[1], maxoff16 = ctx->h_scalars[3];
   const int tier_n[3] = {ctx->h_scalars[4], ctx->h_scalars[5], ctx->h_scalars[6]};
   const int maxoff16_t0 = ctx->h_scalars[7];
+  const int max_m = ctx->h_scalars[16], max_n = ctx->h_scalars[17];
   if (dev_in) {
     tot_r = h_tot[0];
     tot_q = h_tot[1];
   }
-  // packed sequences: guard word + data + guard word per pair (load_word_rw)
-  if ((rc = grow(ctx->rw, 4 * (tot_r / 8 + 4 * P + 4))) || (rc = grow(ctx->qw, 4 * (tot_q / 8 + 4 * P + 4))))
-    return rc;
+  // packing scratch per work unit: guard word + up to len/8 + 2 data words + guard word
+  // (load_word_rw), rounded up to 32 B; the unit count is sized at the launches below
+  const uint64_t rstride = ((uint64_t)max_m / 8 + 4 + 7) & ~7ull, qstride = ((uint64_t)max_n / 8 + 4 + 7) & ~7ull;
   if (err0 & 2) return AGATHA_EEMPTY;
   if (err0 & 4) return AGATHA_ERANGE;
 
@@ -2111,7 +2185,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     mix((uint64_t)(uint32_t)p->gap_extend | ((uint64_t)(uint32_t)p->band_left << 32));
     mix((uint64_t)(uint32_t)p->band_right | ((uint64_t)(uint32_t)p->zdrop << 32));
     mix((uint64_t)(uint32_t)p->variant);
-    mix(tot_r); mix(tot_q);
+    mix(tot_r); mix(tot_q); mix(fed ? (uint64_t)fed->n_owners : 0);
     if (fp == 0) fp = 1;
     queue_fp_kernel<<<1, 1, 0, st>>>(b->queue, fp, (const unsigned long long*)(d_sc + 12), d_sc + 15);
     CUDA_TRY(cudaGetLastError());
@@ -2147,6 +2221,8 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
 
   AlignArgs A;
+  A.rstride = rstride; A.qstride = qstride; A.unit_base = 0;
+  if (fed) A.own = *fed; else A.own.n_owners = 0;
   A.rw = (uint32_t*)ctx->rw.p; A.qw = (uint32_t*)ctx->qw.p;
   A.ref_ascii = d_ref; A.qry_ascii = d_qry; A.chunk_of = (const uint8_t*)ctx->chunk_of.p;
   A.ready = d_ready; A.err_flags = d_sc; A.nmap = nmap ? 1 : 0;
@@ -2185,12 +2261,26 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     }
     CUDA_TRY(cudaEventRecord(ctx->cev[1], ctx->copy_stream));
   }
-  int grid = 0;
+  int grid = 0, units_total = 0;
   int tiers_launched = 0, slots = 0;
   memset(ctx->stats.tier_pairs, 0, sizeof(ctx->stats.tier_pairs));
+  // two passes over the launch selection: the dry one sizes the packing scratch (units of
+  // every launch of this call; the tier launches run together, so theirs are disjoint),
+  // the second launches
+  for (int pass = 0; pass < 2 && !rc; ++pass) {
+  const bool dry = pass == 0;
+  int units = 0;
+  grid = 0; tiers_launched = 0; slots = 0;
+  if (!dry) {
+    if ((rc = grow(ctx->rw, 4 * rstride * (uint64_t)(units_total > 0 ? units_total : 1))) ||
+        (rc = grow(ctx->qw, 4 * qstride * (uint64_t)(units_total > 0 ? units_total : 1))))
+      break;
+    A.rw = (uint32_t*)ctx->rw.p; A.qw = (uint32_t*)ctx->qw.p;
+  }
   if (split) {
-    CUDA_TRY(cudaEventRecord(ctx->tev[0], st));
+    if (!dry) CUDA_TRY(cudaEventRecord(ctx->tev[0], st));
     uint32_t start = 0;
+    int unit_base = 0;
     for (int t = 0; t < 3 && !rc; ++t) {
       if (tier_n[t] == 0) continue;
       AlignArgs At = A;
@@ -2199,43 +2289,50 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
       // a shared queue (NEXT #1) holds one counter per tier, claimed in the same
       // tier-major order by every participant
       At.queue = b->queue ? b->queue + t : (t == 0 ? d_sc + 2 : d_sc + 7 + t);
+      At.unit_base = unit_base;  // the tiers run together: disjoint packing scratch
       start += (uint32_t)tier_n[t];
       cudaStream_t ts = st;
-      if (t > 0) {
+      if (t > 0 && !dry) {
         ts = ctx->tier_stream[t - 1];
         if (cudaStreamWaitEvent(ts, ctx->tev[0], 0) != cudaSuccess) { rc = AGATHA_ECUDA; break; }
       }
-      int g = 0;
-      if (t == 0) rc = launch_align16_wide(ctx, At, ts, &g, maxoff16_t0);
-      else if (t == 1) rc = launch_align16<8, false, NCAP8>(ctx, At, ts, &g);
-      else rc = launch_align16<4, false, 3>(ctx, At, ts, &g);
-      if (t > 0 && !rc && cudaEventRecord(ctx->tev[t], ts) != cudaSuccess) rc = AGATHA_ECUDA;
+      int g = 0, u = 0;
+      if (t == 0) rc = launch_align16_wide(ctx, At, ts, &g, maxoff16_t0, &u, dry);
+      else if (t == 1) rc = launch_align16<8, false, NCAP8>(ctx, At, ts, &g, &u, dry);
+      else rc = launch_align16<4, false, 3>(ctx, At, ts, &g, &u, dry);
+      unit_base += u;
+      units += u;
+      if (t > 0 && !rc && !dry && cudaEventRecord(ctx->tev[t], ts) != cudaSuccess) rc = AGATHA_ECUDA;
       grid += g;
       ++tiers_launched;
       ctx->stats.tier_pairs[t] = tier_n[t];
       if (!slots) slots = 32 >> t;
     }
-    for (int t = 1; t < 3 && !rc; ++t)
+    for (int t = 1; t < 3 && !rc && !dry; ++t)
       if (tier_n[t] && cudaStreamWaitEvent(st, ctx->tev[t], 0) != cudaSuccess) rc = AGATHA_ECUDA;
   } else if (k16) {
     // (NREG = 16) eight capped registers suffice when every pair's low padding
     // off = (-D) mod 16 is at most 8 (prep_kernel's max); else all sixteen
     const int t = tier_of(maxD);
-    if (t == 2) rc = tr ? launch_align16<4, true, 3>(ctx, A, st, &grid) : launch_align16<4, false, 3>(ctx, A, st, &grid);
-    else if (t == 1) rc = tr ? launch_align16<8, true, NCAP8>(ctx, A, st, &grid) : launch_align16<8, false, NCAP8>(ctx, A, st, &grid);
-    else if (tr) rc = launch_align16<16, true, 16>(ctx, A, st, &grid);
-    else rc = launch_align16_wide(ctx, A, st, &grid, maxoff16);
+    int* u = &units;
+    if (t == 2) rc = tr ? launch_align16<4, true, 3>(ctx, A, st, &grid, u, dry) : launch_align16<4, false, 3>(ctx, A, st, &grid, u, dry);
+    else if (t == 1) rc = tr ? launch_align16<8, true, NCAP8>(ctx, A, st, &grid, u, dry) : launch_align16<8, false, NCAP8>(ctx, A, st, &grid, u, dry);
+    else if (tr) rc = launch_align16<16, true, 16>(ctx, A, st, &grid, u, dry);
+    else rc = launch_align16_wide(ctx, A, st, &grid, maxoff16, u, dry);
     tiers_launched = 1;
     ctx->stats.tier_pairs[t] = (int)P;
     slots = 32 >> t;
   } else {
-    if (K == 16) rc = tr ? launch_align<16, true>(ctx, A, st, &grid) : launch_align<16, false>(ctx, A, st, &grid);
-    else if (maxD <= kMaxSlots) rc = tr ? launch_align<32, true>(ctx, A, st, &grid) : launch_align<32, false>(ctx, A, st, &grid);
+    int* u = &units;
+    if (K == 16) rc = tr ? launch_align<16, true>(ctx, A, st, &grid, u, dry) : launch_align<16, false>(ctx, A, st, &grid, u, dry);
+    else if (maxD <= kMaxSlots) rc = tr ? launch_align<32, true>(ctx, A, st, &grid, u, dry) : launch_align<32, false>(ctx, A, st, &grid, u, dry);
     else if (maxD <= 2 * kMaxSlots)  // NEXT #3: wide bands, two or four warps per pair
-      rc = tr ? launch_align_wide<2, true>(ctx, A, st, &grid) : launch_align_wide<2, false>(ctx, A, st, &grid);
-    else rc = tr ? launch_align_wide<4, true>(ctx, A, st, &grid) : launch_align_wide<4, false>(ctx, A, st, &grid);
+      rc = tr ? launch_align_wide<2, true>(ctx, A, st, &grid, u, dry) : launch_align_wide<2, false>(ctx, A, st, &grid, u, dry);
+    else rc = tr ? launch_align_wide<4, true>(ctx, A, st, &grid, u, dry) : launch_align_wide<4, false>(ctx, A, st, &grid, u, dry);
     tiers_launched = 1;
     slots = K;
+  }
+  if (dry) units_total = units;
   }
   ctx->stats.packed16 = k16 ? 1 : 0;
   if (rc) {  // nothing launched may still be using the caller's buffers on return
@@ -2311,7 +2408,7 @@ int agatha_ctx_create(agatha_ctx_t** out, int device) {
   for (int i = 0; i < 3; ++i) cudaEventCreateWithFlags(&ctx->tev[i], cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2; ++i) cudaStreamCreateWithFlags(&ctx->tier_stream[i], cudaStreamNonBlocking);
-  if (cudaMallocHost(&ctx->h_scalars, 64) != cudaSuccess ||
+  if (cudaMallocHost(&ctx->h_scalars, 256) != cudaSuccess ||
       cudaMallocHost(&ctx->h_ones, 4 * kMaxChunks) != cudaSuccess ||
       cudaMallocHost(&ctx->h_chunk_first, 8 * (kMaxChunks + 1)) != cudaSuccess) {
     cudaGetLastError();
@@ -2347,6 +2444,68 @@ void agatha_ctx_destroy(agatha_ctx_t* ctx) {
 int agatha_align_batch(agatha_ctx_t* ctx, const agatha_batch_t* batch, const agatha_params_t* params,
                        agatha_result_t* out, void* stream) {
   return run_batch(ctx, batch, params, out, (cudaStream_t)stream, -1, nullptr, nullptr, 0);
+}
+
+int agatha_align_federated(agatha_ctx_t* ctx, const agatha_batch_t* owners, int n_owners,
+                           const agatha_params_t* params, agatha_result_t* out, int32_t* queue,
+                           uint32_t flags, void* stream) {
+  if (!ctx || !owners || !out || n_owners < 1 || n_owners > kMaxOwners) return AGATHA_EINVAL;
+  Owners O;
+  memset(&O, 0, sizeof(O));
+  O.n_owners = n_owners;
+  uint64_t total = 0;
+  for (int o = 0; o < n_owners; ++o) {
+    const agatha_batch_t& b = owners[o];
+    if (!(b.flags & AGATHA_MEM_DEVICE) || !b.ref || !b.qry || !b.ref_off || !b.qry_off) return AGATHA_EINVAL;
+    if (b.n_pairs == 0) return AGATHA_EEMPTY;
+    O.ref[o] = b.ref; O.qry[o] = b.qry; O.roff[o] = b.ref_off; O.qoff[o] = b.qry_off;
+    O.start[o] = (uint32_t)total;
+    total += b.n_pairs;
+    if (total >= (1ull << 31)) return AGATHA_ERANGE;
+  }
+  O.start[n_owners] = (uint32_t)total;
+  agatha_batch_t g;
+  memset(&g, 0, sizeof(g));
+  g.n_pairs = total;
+  g.flags = (flags & ~(AGATHA_MEM_DEVICE | AGATHA_OUT_DEVICE)) | AGATHA_MEM_DEVICE | AGATHA_OUT_DEVICE;
+  g.queue = queue;
+  return run_batch(ctx, &g, params, out, (cudaStream_t)stream, -1, nullptr, nullptr, 0, &O);
+}
+
+// Device buffers other processes can map (CUDA IPC; over NVLink when on another GPU).
+int agatha_ipc_alloc(agatha_ctx_t* ctx, uint64_t bytes, void** ptr, uint8_t handle[64]) {
+  if (!ctx || !ptr || !handle || bytes == 0) return AGATHA_EINVAL;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  void* q = nullptr;
+  if (cudaMalloc(&q, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return AGATHA_ENOMEM;
+  }
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, q) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(q);
+    return AGATHA_ECUDA;
+  }
+  memcpy(handle, &h, 64);
+  *ptr = q;
+  return AGATHA_OK;
+}
+
+int agatha_ipc_open(agatha_ctx_t* ctx, const uint8_t handle[64], void** ptr) {
+  if (!ctx || !ptr || !handle) return AGATHA_EINVAL;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return AGATHA_OK;
+}
+
+int agatha_ipc_close(agatha_ctx_t* ctx, void* ptr, int opened) {
+  if (!ctx || !ptr) return AGATHA_EINVAL;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(opened ? cudaIpcCloseMemHandle(ptr) : cudaFree(ptr));
+  return AGATHA_OK;
 }
 
 int agatha_localmax_trace(agatha_ctx_t* ctx, const agatha_batch_t* batch, const agatha_params_t* params,
@@ -2421,7 +2580,7 @@ int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* b, const agatha_params_
   pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1; pa.max_off16 = d_sc + 3;
   pa.chunk_first = nullptr; pa.nchunks = 1; pa.chunk_of = nullptr; pa.key64 = nullptr;
   pa.tier_shift = 32; pa.tier_count = nullptr; pa.max_off16_t0 = nullptr; pa.lpt_from = 1;
-  pa.len_hash = nullptr;
+  pa.len_hash = nullptr; pa.own.n_owners = 0; pa.max_len = nullptr;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);
   CUDA_TRY(cudaGetLastError());

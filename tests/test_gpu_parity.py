@@ -604,3 +604,119 @@ def test_shared_queue_two_processes(gpu_lib, ctx):
     rc, exp, _ = oracle.align_batch(pairs, params)
     assert rc == 0
     _check_claims([got[0], got[1]], pairs, params, exp)
+
+
+# NEXT #1 without replicated inputs: a federated batch is the
+# concatenation of several owners' device batches; a claimed pair's inputs are read from
+# its owner's memory (another process's, or over NVLink another GPU's).
+def _dev_owner(pairs):
+    import torch
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return (dev(pairs.ref), dev(pairs.ref_off.view(np.int64)), dev(pairs.qry), dev(pairs.qry_off.view(np.int64)))
+
+
+@pytest.mark.parametrize("name", ["C5", "LS10", "C1"])
+def test_federated_owners_one_context(gpu_lib, ctx, name):
+    import torch
+    cfg = synth.CONFIGS[name]
+    cuts = [0, 70, 71, 300]  # owners of 70, 1 and 229 pairs
+    parts = [synth.generate(cfg, a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+    whole = synth.generate(cfg, 0, cuts[-1])
+    params = vars(cfg.scoring)
+    rc, exp, _ = oracle.align_batch(whole, params)
+    assert rc == 0
+    owners = [_dev_owner(p) for p in parts]
+    for flags in (0, gpu_lib.SINGLE_TIER, gpu_lib.FORCE_32BIT, gpu_lib.ORDER_INPUT):
+        out = torch.zeros(24 * whole.n_pairs, dtype=torch.uint8, device="cuda")
+        gpu_lib.align_federated(ctx, owners, params, out, flags=flags)
+        got = gpu_lib.device_results(out)
+        bad = np.nonzero(got != exp)[0]
+        assert len(bad) == 0, (flags, len(bad), int(bad[0]), got[bad[0]], exp[bad[0]])
+
+
+def _fed_worker(rank, handle_q, result_q, done_q):
+    """One participant: it owns pairs [200 rank, 200 rank + 200) of C5 in its own IPC
+    buffers (its H2D is its own shard), maps the other's, and claims from one queue."""
+    import torch
+    from paper_2403_06478_b200 import agatha
+    torch.cuda.set_device(0)
+    c = agatha.Context(0)
+    cfg = synth.CONFIGS["C5"]
+    mine = synth.generate(cfg, 200 * rank, 200 * rank + 200)
+    arrays = [mine.ref, mine.ref_off.view(np.uint8), mine.qry, mine.qry_off.view(np.uint8)]
+    bufs = []
+    for a in arrays:
+        b = agatha.IpcBuffer.alloc(c, a.nbytes)
+        b.copy_from_host(a)  # H2D: this participant copies only its own shard
+        bufs.append(b)
+    q = agatha.SharedQueue.create(c) if rank == 0 else None
+    handle_q.put((rank, [b.handle for b in bufs], [a.nbytes for a in arrays], q.handle if q else None))
+    peers = {}
+    while len(peers) < 1:
+        item = handle_q.get(timeout=300)
+        if item[0] == rank:  # own message came back: put it back for the other one
+            handle_q.put(item)
+            import time
+            time.sleep(0.05)
+            continue
+        peers[item[0]] = item
+    other = peers[1 - rank]
+    if rank == 1:
+        q = agatha.SharedQueue.open(c, other[3])
+    ob = [agatha.IpcBuffer.open(c, h, n) for h, n in zip(other[1], other[2])]
+
+    def owner(bs, npairs):
+        return (agatha.DevicePtr(bs[0].ptr, bs[0].nbytes), agatha.DevicePtr(bs[1].ptr, npairs + 1),
+                agatha.DevicePtr(bs[2].ptr, bs[2].nbytes), agatha.DevicePtr(bs[3].ptr, npairs + 1))
+
+    owners = [owner(bufs, 200), owner(ob, 200)] if rank == 0 else [owner(ob, 200), owner(bufs, 200)]
+    out = torch.zeros(24 * 400, dtype=torch.uint8, device="cuda")
+    result_q.put(("ready", rank))
+    agatha.align_federated(c, owners, vars(cfg.scoring), out, queue=q)
+    torch.cuda.synchronize()
+    result_q.put((rank, out.cpu().numpy().tobytes()))
+    # rank 0's queue and both processes' buffers are mapped by the other: close only
+    # after both are done
+    done_q.put(rank)
+    seen = {rank}
+    while len(seen) < 2:
+        r = done_q.get(timeout=300)
+        if r in seen:
+            done_q.put(r)
+            import time
+            time.sleep(0.05)
+        seen.add(r)
+    for b in ob:
+        b.close()
+    if rank == 1:
+        q.close()
+    import time
+    time.sleep(1.0)
+    for b in bufs:
+        b.close()
+    if rank == 0:
+        q.close()
+    c.close()
+
+
+def test_federated_two_processes_shared_queue(gpu_lib, ctx):
+    import torch.multiprocessing as tmp
+    mpc = tmp.get_context("spawn")
+    hq, rq, dq = mpc.Queue(), mpc.Queue(), mpc.Queue()
+    ps = [mpc.Process(target=_fed_worker, args=(r, hq, rq, dq)) for r in range(2)]
+    for p_ in ps:
+        p_.start()
+    got = {}
+    while len(got) < 2:
+        item = rq.get(timeout=300)
+        if item[0] != "ready":
+            got[item[0]] = np.frombuffer(item[1], gpu_lib.RESULT_DTYPE)
+    for p_ in ps:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    cfg = synth.CONFIGS["C5"]
+    whole = synth.generate(cfg, 0, 400)
+    params = vars(cfg.scoring)
+    rc, exp, _ = oracle.align_batch(whole, params)
+    assert rc == 0
+    _check_claims([got[0], got[1]], whole, params, exp)
