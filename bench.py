@@ -90,9 +90,10 @@ def parse():
                     help="queue: persistent warps refill from the work queue (default); "
                          "static: warp u takes order positions u, u+W, ... (no-refill ablation)")
     ap.add_argument("--balance", default="static", choices=["static", "dynamic"],
-                    help="static: fixed per-rank shards; dynamic: every rank holds the whole "
-                         "batch and the persistent kernels claim pairs from one counter in "
-                         "rank 0's HBM with system-scope atomics (NEXT #1)")
+                    help="static: fixed per-rank shards; dynamic: every rank holds its shard in "
+                         "IPC-shared HBM, the persistent kernels of all ranks claim pairs of the "
+                         "federated batch from one counter in rank 0's HBM and read a claimed "
+                         "pair from its owner over NVLink (NEXT #1)")
     return ap.parse_args()
 
 
@@ -359,29 +360,48 @@ def main():
                 torch.empty(nq, dtype=torch.uint8, pin_memory=True).numpy())
 
     t0 = time.perf_counter()
-    if dynamic:
-        # every rank holds the whole batch (replicated inputs) and claims pairs at run time
-        shards = None
-        mine = np.arange(n_global, dtype=np.int64)
-        pairs = synth.generate(full, 0, n_global, pinned_out=pinned)
-    else:
-        shards, pairs = rank_shard(full, world, rank, pinned)
-        mine = shards[rank]
+    # every rank holds only its own shard (the LPT partition); in the dynamic mode the
+    # ranks' kernels also claim pairs of the others' shards and read them over NVLink
+    shards, pairs = rank_shard(full, world, rank, pinned)
+    mine = shards[rank]
     gen_s = time.perf_counter() - t0
     params = dict(vars(sc))
-    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    d_ref, d_qry = dev(pairs.ref), dev(pairs.qry)
-    d_roff, d_qoff = dev(pairs.ref_off.view(np.int64)), dev(pairs.qry_off.view(np.int64))
     n_local = pairs.n_pairs
-    pad = n_local if shards is None else max(len(x) for x in shards)
-    d_out_pad = torch.zeros(adist.RECORD_BYTES * pad, dtype=torch.uint8, device="cuda")
-    d_out = d_out_pad[:adist.RECORD_BYTES * n_local]
+    ctx = agatha.Context(local)
+    if dynamic:
+        # NEXT #1: the shard lives in IPC-shareable device buffers; every rank maps the
+        # others' (agatha_ipc_open) and aligns the federated batch (all shards in rank
+        # order) claiming pairs from one counter in rank 0's HBM
+        arrays = (pairs.ref, pairs.ref_off.view(np.uint8), pairs.qry, pairs.qry_off.view(np.uint8))
+        own_bufs = [agatha.IpcBuffer.alloc(ctx, a.nbytes) for a in arrays]
+        for b_, a in zip(own_bufs, arrays):
+            b_.copy_from_host(a)
+        meta = (n_local, [b_.handle for b_ in own_bufs], [a.nbytes for a in arrays])
+        metas = [meta]
+        if world > 1:
+            metas = [None] * world
+            dist.all_gather_object(metas, meta)
+        bufs = [own_bufs if r == rank else [agatha.IpcBuffer.open(ctx, h, nb) for h, nb in zip(metas[r][1], metas[r][2])]
+                for r in range(world)]
+        owners = [(agatha.DevicePtr(bs[0].ptr, bs[0].nbytes), agatha.DevicePtr(bs[1].ptr, metas[r][0] + 1),
+                   agatha.DevicePtr(bs[2].ptr, bs[2].nbytes), agatha.DevicePtr(bs[3].ptr, metas[r][0] + 1))
+                  for r, bs in enumerate(bufs)]
+        fed_order = np.concatenate(shards)  # global row g of the federated batch -> stream pair
+        d_out = torch.zeros(adist.RECORD_BYTES * n_global, dtype=torch.uint8, device="cuda")
+        d_out_pad = d_out
+        pad = n_local
+    else:
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        d_ref, d_qry = dev(pairs.ref), dev(pairs.qry)
+        d_roff, d_qoff = dev(pairs.ref_off.view(np.int64)), dev(pairs.qry_off.view(np.int64))
+        pad = max(len(x) for x in shards)
+        d_out_pad = torch.zeros(adist.RECORD_BYTES * pad, dtype=torch.uint8, device="cuda")
+        d_out = d_out_pad[:adist.RECORD_BYTES * n_local]
     flags = agatha.ORDER_INPUT if args.order == "input" else 0
     if args.tiers == "single":
         flags |= agatha.SINGLE_TIER
     if args.refill == "static":
         flags |= agatha.STATIC_ASSIGN
-    ctx = agatha.Context(local)
     stream = torch.cuda.current_stream()
     queue = None
     if dynamic:  # NEXT #1: one pair counter in rank 0's HBM, mapped by every rank
@@ -402,8 +422,10 @@ def main():
     def step():
         if dynamic:
             start_dynamic()
-        agatha.align_batch(ctx, d_ref, d_roff, d_qry, d_qoff, params, out=d_out, flags=flags,
-                           stream=stream, queue=queue)
+            agatha.align_federated(ctx, owners, params, d_out, queue=queue, flags=flags, stream=stream)
+        else:
+            agatha.align_batch(ctx, d_ref, d_roff, d_qry, d_qoff, params, out=d_out, flags=flags,
+                               stream=stream, queue=queue)
         state["kernel_ms"] = ctx.stats()["align_ms"]
         state["launches"] += ctx.stats()["kernel_launches"]
         if dynamic:
@@ -436,9 +458,12 @@ def main():
     stats = ctx.stats()
     res = agatha.device_results(d_out)
     ms_max = adist.max_over_ranks(ms, "cuda", world)
-    if dynamic:  # res is the merged whole batch; this rank aligned the pairs it claimed
+    if dynamic:  # res is the merged federated batch; this rank aligned the pairs it claimed
         cells_all = float(res["cells"].sum())
         cells_rank = int(state["mine"].item())
+        res_all = np.zeros(n_global, res.dtype)
+        res_all[fed_order] = res  # stream order
+        res = res_all[mine]       # this rank's own pairs (parity sample below)
     else:
         cells_rank = int(res["cells"].sum())
         cells_all = adist.sum_over_ranks(float(cells_rank), "cuda", world)
@@ -464,14 +489,19 @@ def main():
 
         def e2e_step():
             if dynamic:
+                # this rank's shard H2D into its shared buffers (the other ranks read them),
+                # every rank's copy done before any kernel starts (the barrier in start_dynamic)
+                for b_, a in zip(own_bufs, arrays):
+                    b_.copy_from_host(a, stream=stream)
+                stream.synchronize()
                 start_dynamic()
-                agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
-                                   out=host_out, flags=flags, stream=stream, queue=queue)
-                if world > 1:  # merge the ranks' claimed rows
-                    t = torch.from_numpy(host_out.view(np.uint8)).cuda()
-                    adist.merge_claimed(t, world)
-                    host_out.view(np.uint8)[:] = t.cpu().numpy()
-                box["res"] = host_out
+                agatha.align_federated(ctx, owners, params, d_e2e_pad, queue=queue, flags=flags, stream=stream)
+                adist.merge_claimed(d_e2e_pad, world)
+                if rank == 0:
+                    rows = d_e2e_pad.cpu().numpy().view(agatha.RESULT_DTYPE)
+                    out_ = np.zeros(n_global, rows.dtype)
+                    out_[fed_order] = rows
+                    box["res"] = out_
             elif world == 1:
                 agatha.align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
                                    out=host_out, flags=flags, stream=stream)
@@ -491,7 +521,11 @@ def main():
         ev1.record(stream)
         barrier()
         e_ms = adist.max_over_ranks(ev0.elapsed_time(ev1), "cuda", world)
-        if dynamic or world == 1:
+        if dynamic:
+            if rank == 0:
+                assert box["res"].tobytes() == res_all.tobytes()
+            d2h = 24 * n_global if rank == 0 else 0
+        elif world == 1:
             assert box["res"].tobytes() == res.tobytes()
             d2h = 24 * n_local
         else:
@@ -591,7 +625,8 @@ def main():
         mism = int((res[idx] != ores).sum())
         parity = {"pairs_checked": int(len(idx)), "mismatches": mism}
 
-    par = (f"{world} GPU(s) claim pairs from one shared counter (system-scope atomics, NEXT #1)"
+    par = (f"{world} GPU(s) claim pairs of the federated batch from one shared counter (system-scope "
+           "atomics; a stolen pair read from its owner's HBM over NVLink, NEXT #1)"
            if dynamic else (f"LPT partition over nominal cells into {world} shards, NCCL all_gather"
                             if world > 1 else "1 GPU"))
     line = {
