@@ -109,7 +109,24 @@ typedef struct {
                      fingerprint of these (pair count, every pair's lengths, params,
                      flags; not the bases) in the queue; a participant whose fingerprint
                      differs returns AGATHA_EINVAL before claiming any pair.          */
+  struct agatha_ends* ends; /* NULL, or n_pairs end-score records (NEXT #4, below) on the
+                     same side as `out` (AGATHA_OUT_DEVICE), written in pair order  */
 } agatha_batch_t;
+
+/* NEXT #4 (minimap2's mqe / mte / end score, outside the paper; DESIGN.md
+ * reading R19): over the cells the sweep processed (anti-diagonals 2 .. c_end, c_end the
+ * Z-drop anti-diagonal or m + n), in anti-diagonal order with a strict '>':
+ *   mqe = max H(i, n) (the query end reached) and its i (smallest on ties);
+ *   mte = max H(m, j) (the reference end reached) and its j;
+ *   end_score = H(m, n) when that cell was processed.
+ * An absent value is AGATHA_NO_SCORE with position -1.  24 bytes. */
+#define AGATHA_NO_SCORE (-(1 << 30))
+typedef struct agatha_ends {
+  int32_t mqe, mqe_i;
+  int32_t mte, mte_j;
+  int32_t end_score;
+  int32_t reserved;
+} agatha_ends_t;
 
 /* Per-pair result: 24 bytes, written in pair order. */
 typedef struct {

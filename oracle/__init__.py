@@ -100,6 +100,12 @@ def _load() -> ctypes.CDLL:
                                            ctypes.c_void_p, ctypes.c_uint64,
                                            ctypes.POINTER(Params), ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_int]
+        lib.oracle_align_one_ends.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_char_p,
+                                              ctypes.c_int64, ctypes.POINTER(Params),
+                                              ctypes.POINTER(_Result), ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_align_batch_ends.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(Params),
+                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         lib.oracle_nominal_cells.argtypes = [ctypes.c_int64] * 4
         lib.oracle_nominal_cells.restype = ctypes.c_int64
         lib.oracle_pack4.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_void_p,
@@ -149,6 +155,44 @@ def align_batch(pairs, params, threads: Optional[int] = None):
                                     qry_off.ctypes.data, n, ctypes.byref(p), out.ctypes.data,
                                     status.ctypes.data, threads or (os.cpu_count() or 1))
     return rc, out, status
+
+
+# NEXT #4 end scores (reading R19): mqe / mqe_i (query end), mte / mte_j (reference end),
+# end_score = H(m, n); absent -> NO_SCORE and position -1.
+ENDS_DTYPE = np.dtype([("mqe", "<i4"), ("mqe_i", "<i4"), ("mte", "<i4"), ("mte_j", "<i4"),
+                       ("end_score", "<i4"), ("reserved", "<i4")])
+NO_SCORE = -(1 << 30)
+
+
+def align_one_ends(R, Q, params):
+    """``(rc, result_tuple, ends_tuple)`` for one pair (ends = mqe, mqe_i, mte, mte_j, end_score)."""
+    R, Q = _b(R), _b(Q)
+    p = params_from(params)
+    res = _Result()
+    ends = np.zeros(1, ENDS_DTYPE)
+    rc = _load().oracle_align_one_ends(R, len(R), Q, len(Q), ctypes.byref(p), ctypes.byref(res), None,
+                                       ends.ctypes.data)
+    out = (res.score, res.ref_end, res.query_end, res.zdrop_antidiag, res.cells)
+    return rc, out, tuple(ends[0].tolist())[:5]
+
+
+def align_batch_ends(pairs, params, threads: Optional[int] = None):
+    """align_batch plus each pair's end scores: ``(rc, results, ends, status)``."""
+    p = params_from(params)
+    n = pairs.n_pairs
+    out = np.zeros(n, RESULT_DTYPE)
+    ends = np.zeros(n, ENDS_DTYPE)
+    status = np.zeros(n, np.int32)
+    if n == 0:
+        return EEMPTY, out, ends, status
+    ref_off = np.ascontiguousarray(pairs.ref_off, np.uint64)
+    qry_off = np.ascontiguousarray(pairs.qry_off, np.uint64)
+    ref = np.ascontiguousarray(pairs.ref, np.uint8)
+    qry = np.ascontiguousarray(pairs.qry, np.uint8)
+    rc = _load().oracle_align_batch_ends(ref.ctypes.data, ref_off.ctypes.data, qry.ctypes.data,
+                                         qry_off.ctypes.data, n, ctypes.byref(p), out.ctypes.data,
+                                         ends.ctypes.data, status.ctypes.data, threads or (os.cpu_count() or 1))
+    return rc, out, ends, status
 
 
 def nominal_cells(m: int, n: int, band_left: int, band_right: int) -> int:

@@ -63,6 +63,21 @@ typedef struct {
   int64_t cells;          /* in-band in-table cells on anti-diagonals 2..end  */
 } oracle_result_t;
 
+/* NEXT #4 (minimap2 semantics, outside the paper; reading R19):
+ * the end scores over the cells the sweep processed (anti-diagonals 2..c_end, c_end the
+ * Z-drop anti-diagonal or m+n), updated in anti-diagonal order with a strict '>':
+ *   mqe = max H(i, n) (the query end reached), mqe_i its i (the smallest on ties);
+ *   mte = max H(m, j) (the reference end reached), mte_j its j;
+ *   end_score = H(m, n) if that cell was processed.
+ * Absent values are ORACLE_NO_SCORE with position -1. */
+#define ORACLE_NO_SCORE (-(1 << 30))
+typedef struct {
+  int32_t mqe, mqe_i;
+  int32_t mte, mte_j;
+  int32_t end_score;
+  int32_t reserved;
+} oracle_ends_t;
+
 enum {
   ORACLE_OK = 0,
   ORACLE_EINVAL = -1,
@@ -143,8 +158,17 @@ typedef struct {
   int64_t cap;
 } oracle_trace_t;
 
+int oracle_align_one_ends(const uint8_t* R, int64_t m, const uint8_t* Q, int64_t n,
+                          const oracle_params_t* p, oracle_result_t* out, oracle_trace_t* trace,
+                          oracle_ends_t* ends);
 int oracle_align_one(const uint8_t* R, int64_t m, const uint8_t* Q, int64_t n,
                      const oracle_params_t* p, oracle_result_t* out, oracle_trace_t* trace) {
+  return oracle_align_one_ends(R, m, Q, n, p, out, trace, NULL);
+}
+
+int oracle_align_one_ends(const uint8_t* R, int64_t m, const uint8_t* Q, int64_t n,
+                          const oracle_params_t* p, oracle_result_t* out, oracle_trace_t* trace,
+                          oracle_ends_t* ends) {
   int rc = oracle_validate(p);
   if (rc) return rc;
   if (m <= 0 || n <= 0) return ORACLE_EEMPTY;
@@ -182,6 +206,8 @@ int oracle_align_one(const uint8_t* R, int64_t m, const uint8_t* Q, int64_t n,
   const int gate_ge = (p->variant & VAR_GATE_GE) != 0;
   const int64_t c_check_end = (p->variant & VAR_CHECK_LAST) ? m + n + 1 : m + n;
   int64_t term = -1, cells = 0;
+  oracle_ends_t en = {ORACLE_NO_SCORE, -1, ORACLE_NO_SCORE, -1, ORACLE_NO_SCORE, 0};
+  int have_q = 0, have_t = 0;
 
   /* step 4: c = 2, 3, ..., m+n */
   for (int64_t c = 2; c <= m + n; ++c) {
@@ -208,6 +234,10 @@ int oracle_align_one(const uint8_t* R, int64_t m, const uint8_t* Q, int64_t n,
       s.E0[i] = e;
       s.F0[i] = f;
       ++cells;
+      /* NEXT #4: end scores of this processed cell (reading R19) */
+      if (j == n && (!have_q || h > en.mqe)) { en.mqe = h; en.mqe_i = (int32_t)i; have_q = 1; }
+      if (i == m && (!have_t || h > en.mte)) { en.mte = h; en.mte_j = (int32_t)j; have_t = 1; }
+      if (i == m && j == n) en.end_score = h;
       /* 4c: local max (Eq. 5), ties -> smallest i (ascending scan, strict >) */
       if (!any || h > L_H) { L_H = h; L_i = i; }
       any = 1;
@@ -243,6 +273,7 @@ int oracle_align_one(const uint8_t* R, int64_t m, const uint8_t* Q, int64_t n,
   out->query_end = (int32_t)G_j;
   out->zdrop_antidiag = (int32_t)term;
   out->cells = cells;
+  if (ends) *ends = en;
   return ORACLE_OK;
 }
 
@@ -287,6 +318,7 @@ typedef struct {
   const uint64_t *ref_off, *qry_off;
   const oracle_params_t* p;
   oracle_result_t* out;
+  oracle_ends_t* ends;
   int32_t* status;
   const uint64_t* order;
   uint64_t n;
@@ -304,8 +336,8 @@ static void* batch_worker(void* arg) {
     const uint64_t k = j->order[t];
     const int64_t m = (int64_t)(j->ref_off[k + 1] - j->ref_off[k]);
     const int64_t n = (int64_t)(j->qry_off[k + 1] - j->qry_off[k]);
-    j->status[k] = oracle_align_one(j->ref + j->ref_off[k], m, j->qry + j->qry_off[k], n, j->p,
-                                    &j->out[k], NULL);
+    j->status[k] = oracle_align_one_ends(j->ref + j->ref_off[k], m, j->qry + j->qry_off[k], n, j->p,
+                                         &j->out[k], NULL, j->ends ? &j->ends[k] : NULL);
   }
   return NULL;
 }
@@ -319,9 +351,19 @@ static int cmp_desc(const void* a, const void* b) {
 
 /* Align pairs 0..n_pairs-1; status[k] receives each pair's return code.  Returns
  * the first non-zero status (or 0). */
+int oracle_align_batch_ends(const uint8_t* ref, const uint64_t* ref_off, const uint8_t* qry,
+                            const uint64_t* qry_off, uint64_t n_pairs, const oracle_params_t* p,
+                            oracle_result_t* out, oracle_ends_t* ends, int32_t* status, int n_threads);
 int oracle_align_batch(const uint8_t* ref, const uint64_t* ref_off, const uint8_t* qry,
                        const uint64_t* qry_off, uint64_t n_pairs, const oracle_params_t* p,
                        oracle_result_t* out, int32_t* status, int n_threads) {
+  return oracle_align_batch_ends(ref, ref_off, qry, qry_off, n_pairs, p, out, NULL, status, n_threads);
+}
+
+/* The same, also writing each pair's end scores to ends[k] (NEXT #4) when ends != NULL. */
+int oracle_align_batch_ends(const uint8_t* ref, const uint64_t* ref_off, const uint8_t* qry,
+                            const uint64_t* qry_off, uint64_t n_pairs, const oracle_params_t* p,
+                            oracle_result_t* out, oracle_ends_t* ends, int32_t* status, int n_threads) {
   if (n_pairs == 0) return ORACLE_EEMPTY;
   int rc = oracle_validate(p);
   if (rc) return rc;
@@ -336,7 +378,7 @@ int oracle_align_batch(const uint8_t* ref, const uint64_t* ref_off, const uint8_
   qsort(order, n_pairs, sizeof(uint64_t), cmp_desc);
   batch_job_t job;
   job.ref = ref; job.qry = qry; job.ref_off = ref_off; job.qry_off = qry_off; job.p = p;
-  job.out = out; job.status = status; job.order = order; job.n = n_pairs; job.next = 0;
+  job.out = out; job.ends = ends; job.status = status; job.order = order; job.n = n_pairs; job.next = 0;
   pthread_mutex_init(&job.mu, NULL);
   if (n_threads < 1) n_threads = 1;
   if (n_threads > 512) n_threads = 512;

@@ -112,3 +112,33 @@ def align(R: str, Q: str, match=2, mismatch=4, ambig=None, gap_open=4, gap_exten
     """Full result tuple (score, ref_end, query_end, zdrop_antidiag, cells) by brute force."""
     table = path_table(R, Q, match, mismatch, ambig, gap_open, gap_extend, band_left, band_right)
     return result_from_table(table, len(R), len(Q), band_left, band_right, gap_extend, zdrop, variant)
+
+
+NO_SCORE = -(1 << 30)
+
+
+def ends_from_table(table, m: int, n: int, c_end: int):
+    """NEXT #4 end scores (reading R19) from a table of H values: over the in-band
+    cells with i + j <= c_end, mqe = max H(i, n) (smallest i on ties), mte = max H(m, j)
+    (smallest j on ties), end_score = H(m, n); absent -> (NO_SCORE, -1)."""
+    q = [(table[(i, n)], i) for i in range(1, m + 1) if (i, n) in table and i + n <= c_end]
+    t = [(table[(m, j)], j) for j in range(1, n + 1) if (m, j) in table and m + j <= c_end]
+    mqe, mqe_i = (NO_SCORE, -1)
+    if q:
+        mqe = max(v for v, _ in q)
+        mqe_i = min(i for v, i in q if v == mqe)
+    mte, mte_j = (NO_SCORE, -1)
+    if t:
+        mte = max(v for v, _ in t)
+        mte_j = min(j for v, j in t if v == mte)
+    end = table[(m, n)] if (m, n) in table and m + n <= c_end else NO_SCORE
+    return (mqe, mqe_i, mte, mte_j, end)
+
+
+def align_ends(R: str, Q: str, match=2, mismatch=4, ambig=None, gap_open=4, gap_extend=2,
+               band_left=-1, band_right=-1, zdrop=-1, variant=0):
+    """(result tuple, end-score tuple) by brute force."""
+    table = path_table(R, Q, match, mismatch, ambig, gap_open, gap_extend, band_left, band_right)
+    res = result_from_table(table, len(R), len(Q), band_left, band_right, gap_extend, zdrop, variant)
+    c_end = res[3] if res[3] >= 0 else len(R) + len(Q)
+    return res, ends_from_table(table, len(R), len(Q), c_end)

@@ -48,7 +48,7 @@ VAR_GATE_GE, VAR_ORIGIN_MAX, VAR_CHECK_LAST = 1, 2, 4
 class Batch(ctypes.Structure):
     _fields_ = [("ref", ctypes.c_void_p), ("qry", ctypes.c_void_p), ("ref_off", ctypes.c_void_p),
                 ("qry_off", ctypes.c_void_p), ("n_pairs", ctypes.c_uint64),
-                ("flags", ctypes.c_uint32), ("queue", ctypes.c_void_p)]
+                ("flags", ctypes.c_uint32), ("queue", ctypes.c_void_p), ("ends", ctypes.c_void_p)]
 
 
 class Stats(ctypes.Structure):
@@ -318,8 +318,14 @@ def make_batch(ref, ref_off, qry, qry_off, flags: int = 0) -> Batch:
     return Batch(_ptr(ref), _ptr(qry), _ptr(ref_off), _ptr(qry_off), n_pairs, flags)
 
 
+# NEXT #4 end scores (agatha_ends_t): mqe / mqe_i, mte / mte_j, end_score; absent -> NO_SCORE, -1
+ENDS_DTYPE = np.dtype([("mqe", "<i4"), ("mqe_i", "<i4"), ("mte", "<i4"), ("mte_j", "<i4"),
+                       ("end_score", "<i4"), ("reserved", "<i4")])
+NO_SCORE = -(1 << 30)
+
+
 def align_batch(ctx: Context, ref, ref_off, qry, qry_off, params, out=None, flags: int = 0,
-                stream=None, queue: Optional["SharedQueue"] = None):
+                stream=None, queue: Optional["SharedQueue"] = None, ends=None):
     """agatha_align_batch.  Returns ``out`` (a numpy RESULT_DTYPE array for host outputs,
     or the given CUDA uint8/int tensor of 24*n_pairs bytes for device outputs).  With a
     ``queue`` (SharedQueue) only the pairs this call claims are aligned; the other rows of
@@ -327,6 +333,8 @@ def align_batch(ctx: Context, ref, ref_off, qry, qry_off, params, out=None, flag
     b = make_batch(ref, ref_off, qry, qry_off, flags)
     if queue is not None:
         b.queue = queue.ptr
+    if ends is not None:  # same side as `out`: numpy ENDS_DTYPE array, or CUDA bytes
+        b.ends = _ptr(ends)
     p = params_from(params)
     if out is None:
         out = np.zeros(b.n_pairs, RESULT_DTYPE)
@@ -343,6 +351,14 @@ def align_pairs(ctx: Context, pairs, params, flags: int = 0, stream=None):
     """Convenience: align a ``synth.Pairs``-like object (host arrays)."""
     return align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
                        flags=flags, stream=stream)
+
+
+def align_pairs_ends(ctx: Context, pairs, params, flags: int = 0, stream=None):
+    """align_pairs plus the NEXT #4 end scores: ``(results, ends)`` (host arrays)."""
+    ends = np.zeros(pairs.n_pairs, ENDS_DTYPE)
+    res = align_batch(ctx, pairs.ref, pairs.ref_off, pairs.qry, pairs.qry_off, params,
+                      flags=flags, stream=stream, ends=ends)
+    return res, ends
 
 
 def align_pairs_q(ctx: Context, pairs, params, out, queue: "SharedQueue", stream=None, flags: int = 0):

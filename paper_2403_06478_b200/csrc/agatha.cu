@@ -111,6 +111,7 @@ struct AlignArgs {
   const uint32_t* order;     // dispatch order (a2)
   const uint8_t* bad;        // per-pair validation flag from the prep kernel
   agatha_result_t* out;
+  agatha_ends_t* ends;       // NEXT #4: end scores per pair (device), or null
   int* queue;                // global work counter (a7)
   int sysq;                  // 1: the counter is shared across GPUs/processes (system scope)
   int static_assign;         // 1: no queue, unit u takes positions u + k * nunits (ablation)
@@ -139,6 +140,37 @@ struct AlignArgs {
 __device__ __forceinline__ int claim_next(const AlignArgs& A, int unit, int nunits, int& k) {
   if (A.static_assign) return unit + (k++) * nunits;
   return A.sysq ? atomicAdd_system(A.queue, 1) : atomicAdd(A.queue, 1);
+}
+
+// ---- NEXT #4: end scores (agatha_ends_t; reading R19) -------------------------
+// A per-warp (per-block in the wide tier) record in shared memory: e[0..1] mqe, mqe_i,
+// e[2..3] mte, mte_j, e[4] end score.  Each processed anti-diagonal c holds at most one
+// cell with j = n and one with i = m, found by the lane that holds them; anti-diagonals
+// are processed in order, so a strict '>' keeps the earliest (smallest i / j) on ties.
+__device__ __forceinline__ void ends_init(int* e) {
+  e[0] = AGATHA_NO_SCORE; e[1] = -1; e[2] = AGATHA_NO_SCORE; e[3] = -1; e[4] = AGATHA_NO_SCORE;
+}
+__device__ __forceinline__ void ends_cell(int* e, int i, int j, int h, int m, int n) {
+  if (j == n && h > e[0]) { e[0] = h; e[1] = i; }
+  if (i == m && h > e[2]) { e[2] = h; e[3] = j; }
+  if (i == m && j == n) e[4] = h;
+}
+__device__ __forceinline__ void ends_store(agatha_ends_t* dst, const int* e) {
+  agatha_ends_t r;
+  r.mqe = e[0]; r.mqe_i = e[1]; r.mte = e[2]; r.mte_j = e[3]; r.end_score = e[4]; r.reserved = 0;
+  *dst = r;
+}
+// The end cells of anti-diagonal c among this lane's cells t = 0..nc-1 at (ib + t, jb - t):
+// cell t_q has j = n, t_t has i = m.  valid(t): the cell's slot lies in the band.
+template <typename ValueOf, typename Valid>
+__device__ __forceinline__ void ends_capture(int* e, int ib, int jb, int nc, int m, int n,
+                                             ValueOf value_of, Valid valid) {
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    const int t = w == 0 ? jb - n : m - ib;
+    const int i = ib + t, j = jb - t;
+    if (t >= 0 && t < nc && i >= 1 && i <= m && j >= 1 && j <= n && valid(t)) ends_cell(e, i, j, value_of(t), m, n);
+  }
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -357,12 +389,12 @@ __device__ __forceinline__ int step_cells(int (&H)[K], int (&Eh)[K], int (&Fh)[K
 }
 
 template <int K, bool TRACE>
-__device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane, int unit) {
+__device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane, int unit, int* erec) {
   const PairSrc ps = pair_src(A.own, A.ref_ascii, A.qry_ascii, A.roff, A.qoff, pid);
   const uint64_t r0 = ps.r0, q0 = ps.q0;
   const int m = (int)ps.m;
   const int n = (int)ps.n;
-  if (A.bad[pid]) {
+  if (A.bad[pid]) {  // (the call fails; the rows are zero)
     if (lane == 0) {
       agatha_result_t z = {0, 0, 0, -1, 0};
       A.out[pid] = z;
@@ -425,6 +457,25 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane, int unit)
   const uint32_t T0 = A.T0, T1 = A.T1;
   int lk_prev = kNegKey, rH_prev = kEmptyH - 1;  // nothing pending before the first step
   bool stop = false;
+  if (A.ends) {
+    if (lane == 0) ends_init(erec);
+    __syncwarp();
+  }
+  // NEXT #4: the end cells of processed anti-diagonal c (slot parity P, still in H)
+  auto capture = [&](int c, int P) {
+    const int uc = (c - P + dlo) >> 1;
+    const int ib = uc + P + lane * (K / 2), jb = uc - dlo - lane * (K / 2);
+    ends_capture(erec, ib, jb, K / 2, m, n,
+                 [&](int t) {
+                   int v = 0;
+#pragma unroll
+                   for (int k = 0; k < K / 2; ++k)
+                     if (k == t) v = P ? H[1 + 2 * k] : H[2 * k];
+                   return v;
+                 },
+                 [&](int t) { return gbase + P + 2 * t < D; });
+    __syncwarp();
+  };
 
   auto iteration = [&](auto masked_tag) {
     constexpr bool MASKED = decltype(masked_tag)::value;
@@ -449,6 +500,7 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane, int unit)
       }
       const int lk = step_cells<K, 0, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi, A.sixteen);
       const int rH = __reduce_max_sync(kFull, lk >> 4);
+      if (MASKED && A.ends) capture(cb - 1, 1);
       if (process_antidiag<K, 1, TRACE>(s, A, cb - 1, lk_prev, rH_prev, lane, pid)) { stop = true; return; }
       lk_prev = lk;
       rH_prev = rH;
@@ -469,6 +521,7 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane, int unit)
       }
       const int lk = step_cells<K, 1, MASKED>(H, Eh, Fh, S, lane, nalpha, nbeta, capT, tlo, thi, A.sixteen);
       const int rH = __reduce_max_sync(kFull, lk >> 4);
+      if (MASKED && A.ends) capture(cb, 0);
       if (process_antidiag<K, 0, TRACE>(s, A, cb, lk_prev, rH_prev, lane, pid)) { stop = true; return; }
       lk_prev = lk;
       rH_prev = rH;
@@ -488,13 +541,18 @@ __device__ void align_pair(const AlignArgs& A, uint32_t pid, int lane, int unit)
     }
   };
 
+  // with end scores, the steady phase stops before anti-diagonal ce (the first that can
+  // hold an end cell), so that every end cell is processed by a masked step
+  const int ce_steady = A.ends ? ce - 1 : ce;
   while (!stop && cb <= c_last && cb < cs) iteration(TrueT{});
-  while (!stop && cb + 1 <= ce) iteration(FalseT{});
+  while (!stop && cb + 1 <= ce_steady) iteration(FalseT{});
   while (!stop && cb <= c_last) iteration(TrueT{});
   if (!stop) {
     // the last computed step (cb - 1, slot parity 1) is still pending
+    if (A.ends) capture(cb - 1, 1);
     process_antidiag<K, 1, TRACE>(s, A, cb - 1, lk_prev, rH_prev, lane, pid);
   }
+  if (A.ends && lane == 0) ends_store(A.ends + pid, erec);
 
   // a8: cells = in-band in-table cells on anti-diagonals 2 .. c_end (closed form per slot)
   const int c_end = s.term >= 0 ? s.term : m + n;
@@ -529,6 +587,7 @@ struct MinBlocks { static constexpr int value = K >= 32 ? 3 : 4; };
 
 template <int K, bool TRACE>
 __global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignArgs A) {
+  __shared__ int erec_all[4][8];  // NEXT #4 end-score records, one per warp
   const int lane = threadIdx.x & 31;
   const int unit = blockIdx.x * 4 + (threadIdx.x >> 5), nunits = gridDim.x * 4;
   int k = 0;
@@ -537,7 +596,7 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignAr
     if (lane == 0) q = claim_next(A, unit, nunits, k);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
-    align_pair<K, TRACE>(A, A.order[q], lane, unit);
+    align_pair<K, TRACE>(A, A.order[q], lane, unit, erec_all[threadIdx.x >> 5]);
   }
 }
 
@@ -551,6 +610,7 @@ __global__ void __launch_bounds__(128, MinBlocks<K>::value) align_kernel(AlignAr
 // from the block-wide values, identically in all warps, so control flow stays
 // block-uniform.  Same cells, same arithmetic, same results as align_kernel.
 struct WideShared {
+  int ends[8];                                     // NEXT #4 end-score record of the pair
   int up_H[kMaxWarpsWide], up_E[kMaxWarpsWide];   // lane 31's slot K-1 after a PAR = 1 step
   int dn_H[kMaxWarpsWide], dn_F[kMaxWarpsWide];   // lane 0's slot 0 after a PAR = 0 step
   int rH[2][kMaxWarpsWide], d[2][kMaxWarpsWide];  // per step parity: warp max, its diagonal
@@ -661,6 +721,24 @@ __device__ void align_pair_wide(const AlignArgs& A, uint32_t pid, int lane, int 
            Wq2 = load_word_rw(Qw, wQ + 2, nwQ);
   const uint32_t T0 = A.T0, T1 = A.T1;
   bool stop = false;
+  if (A.ends) {
+    if (gl == 0) ends_init(sh.ends);
+    __syncthreads();
+  }
+  // NEXT #4: the end cells of anti-diagonal c (slot parity P, just computed)
+  auto capture = [&](int c, int P) {
+    const int uc = (c - P + dlo) >> 1;
+    const int ib = uc + P + gl * (K / 2), jb = uc - dlo - gl * (K / 2);
+    ends_capture(sh.ends, ib, jb, K / 2, m, n,
+                 [&](int t) {
+                   int v = 0;
+#pragma unroll
+                   for (int k = 0; k < K / 2; ++k)
+                     if (k == t) v = P ? H[1 + 2 * k] : H[2 * k];
+                   return v;
+                 },
+                 [&](int t) { return gbase + P + 2 * t < D; });
+  };
 
   // warp max and the diagonal of its first maximal cell (smallest lane, then slot)
   auto publish = [&](int lk, int par) {
@@ -714,6 +792,10 @@ __device__ void align_pair_wide(const AlignArgs& A, uint32_t pid, int lane, int 
       __syncthreads();
       int rH, d;
       combine_warps(0, rH, d);
+      if (MASKED && A.ends) {
+        capture(cb, 0);
+        __syncthreads();
+      }
       if (process_wide<TRACE>(s, A, cb, rH, d, gl == 0, pid)) { stop = true; return; }
     }
     // ---- step PAR = 1, anti-diagonal cb + 1 ----
@@ -739,6 +821,10 @@ __device__ void align_pair_wide(const AlignArgs& A, uint32_t pid, int lane, int 
       __syncthreads();
       int rH, d;
       combine_warps(1, rH, d);
+      if (MASKED && A.ends) {
+        capture(cb + 1, 1);
+        __syncthreads();
+      }
       if (process_wide<TRACE>(s, A, cb + 1, rH, d, gl == 0, pid)) { stop = true; return; }
     }
     cb += 2;
@@ -755,9 +841,14 @@ __device__ void align_pair_wide(const AlignArgs& A, uint32_t pid, int lane, int 
     }
   };
 
+  const int ce_steady = A.ends ? ce - 1 : ce;  // every end cell in a masked step (NEXT #4)
   while (!stop && cb <= c_last && cb < cs) iteration(TrueT{});
-  while (!stop && cb + 1 <= ce) iteration(FalseT{});
+  while (!stop && cb + 1 <= ce_steady) iteration(FalseT{});
   while (!stop && cb <= c_last) iteration(TrueT{});
+  if (A.ends) {
+    __syncthreads();
+    if (gl == 0) ends_store(A.ends + pid, sh.ends);
+  }
 
   // a8: cells on anti-diagonals 2 .. c_end (closed form per slot), summed over the block
   const int c_end = s.term >= 0 ? s.term : m + n;
@@ -1208,9 +1299,9 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
 #endif
 }
 
-template <int NREG, bool TRACE, int NCAP>
+template <int NREG, bool TRACE, int NCAP, bool ENDS = false>
 __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap, uint32_t* pref,
-                             int unit) {
+                             int unit, int* erec) {
   constexpr int K = 2 * NREG;        // slots per lane
   constexpr int NC = NREG;           // cells per step per lane (K/2)
   const PairSrc ps = pair_src(A.own, A.ref_ascii, A.qry_ascii, A.roff, A.qoff, pid);
@@ -1387,6 +1478,31 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   // The R window shifted for the PAR = 1 step (4*oR + 4) is the next iteration's PAR = 0
   // shift (oR advances by one), also across a refill: the clamped shift by 32 returns
   // the second word, which the refill makes the first.
+  // NEXT #4: the end cells of processed anti-diagonal c (slot parity P, registers still
+  // intact, relative to the base Bc of their step)
+  if (ENDS) {
+    if (lane == 0) ends_init(erec);
+    __syncwarp();
+  }
+  auto capture = [&](int c, int P, int Bc) {
+    const int uc = (c - P + dls) >> 1;
+    const int ib = uc + P + lane * NC, jb = uc - dls - lane * NC;
+    ends_capture(erec, ib, jb, NC, m, n,
+                 [&](int t) {
+                   const int tk = t % (NC / 2);
+                   uint32_t v = 0;
+#pragma unroll
+                   for (int k = 0; k < NREG / 2; ++k)
+                     if (k == tk) v = P ? H[1 + 2 * k] : H[2 * k];
+                   const int st = t >= NC / 2 ? hi16(v) : lo16(v);
+                   return st - alpha * c + Bc;  // stored = X + alpha*c - B
+                 },
+                 [&](int t) {
+                   const int g = K * lane + (t >= NC / 2 ? NREG : 0) + P + 2 * (t % (NC / 2));
+                   return g >= off && g < gend;
+                 });
+    __syncwarp();
+  };
   constexpr bool kRReuse = NREG >= 16 ? AGATHA_RREUSE : AGATHA_RREUSE_NARROW;
   uint32_t rsc[2] = {0u, 0u};
   rshift(rsc, 4 * oR);
@@ -1421,6 +1537,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
       const int lmax = step16<NREG, NCAP, 0, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
       const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
+      if (MASKED && ENDS) capture(cb - 1, 1, B_prev);
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
       if (!AGATHA_STEADYC || MASKED) {
@@ -1452,6 +1569,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       }
       const int lmax = step16<NREG, NCAP, 1, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
       const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
+      if (MASKED && ENDS) capture(cb, 0, B_prev);
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
       if (!AGATHA_STEADYC || MASKED) {
@@ -1531,10 +1649,17 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   {
     const int head_end = min(cs, c_last + 1);                 // head: cb < cs (and cb <= c_last)
     run_phase(TrueT{}, cb < head_end ? (head_end - cb + 1) >> 1 : 0);
-    run_phase(FalseT{}, cb + 1 <= ce ? ((ce - cb + 1) >> 1) : 0);  // steady: cb + 1 <= ce
+    // steady: cb + 1 <= ce; with end scores it stops before ce, the first anti-diagonal
+    // that can hold an end cell, so every end cell is processed by a masked step
+    const int ce_s = ENDS ? ce - 1 : ce;
+    run_phase(FalseT{}, cb + 1 <= ce_s ? ((ce_s - cb + 1) >> 1) : 0);
     run_phase(TrueT{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);  // tail: cb <= c_last
   }
-  if (!stop) process16<NREG, 1, TRACE, false>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
+  if (!stop) {
+    if (ENDS) capture(cb - 1, 1, B_prev);
+    process16<NREG, 1, TRACE, false>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
+  }
+  if (ENDS && lane == 0) ends_store(A.ends + pid, erec);
   resolve_G16<NREG>(s, snap, lane);
 
   const int c_end = s.term >= 0 ? s.term : m + n;
@@ -1590,10 +1715,11 @@ template <int NREG> struct Front16 {
 #ifndef AGATHA_MAXNREG16
 #define AGATHA_MAXNREG16 0
 #endif
-template <int NREG, bool TRACE, int NCAP>
+template <int NREG, bool TRACE, int NCAP, bool ENDS = false>
 __device__ __forceinline__ void align16_body(const AlignArgs& A) {
   __shared__ uint32_t snap_all[Front16<NREG>::wpb][NREG / 2 * 32];
   __shared__ uint32_t pref_all[Front16<NREG>::wpb][64];
+  __shared__ int erec_all[Front16<NREG>::wpb][8];  // NEXT #4 end-score records
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int unit = blockIdx.x * Front16<NREG>::wpb + warp, nunits = gridDim.x * Front16<NREG>::wpb;
   int k = 0;
@@ -1602,19 +1728,19 @@ __device__ __forceinline__ void align16_body(const AlignArgs& A) {
     if (lane == 0) q = claim_next(A, unit, nunits, k);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
-    align_pair16<NREG, TRACE, NCAP>(A, A.order[q], lane, snap_all[warp], pref_all[warp], unit);
+    align_pair16<NREG, TRACE, NCAP, ENDS>(A, A.order[q], lane, snap_all[warp], pref_all[warp], unit, erec_all[warp]);
   }
 }
 
-template <int NREG, bool TRACE, int NCAP>
+template <int NREG, bool TRACE, int NCAP, bool ENDS = false>
 __global__ void __launch_bounds__(32 * Front16<NREG>::wpb, Front16<NREG>::minb) align16_kernel(AlignArgs A) {
-  align16_body<NREG, TRACE, NCAP>(A);
+  align16_body<NREG, TRACE, NCAP, ENDS>(A);
 }
 
 #if AGATHA_MAXNREG16
-template <int NREG, bool TRACE, int NCAP>
+template <int NREG, bool TRACE, int NCAP, bool ENDS = false>
 __global__ void __maxnreg__(AGATHA_MAXNREG16) align16w_kernel(AlignArgs A) {
-  align16_body<NREG, TRACE, NCAP>(A);
+  align16_body<NREG, TRACE, NCAP, ENDS>(A);
 }
 #endif
 
@@ -1877,7 +2003,7 @@ void score_table16(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
   *T1 = t[4] | (t[5] << 8) | (t[6] << 16) | ((uint32_t)t[7] << 24);
 }
 
-template <int NREG, bool TRACE, int NCAP>
+template <int NREG, bool TRACE, int NCAP, bool ENDS = false>
 int occupancy16() {  // resident blocks per SM
   // cached per instantiation; contexts on several host threads may race to fill it
   // (they compute the same value), so the cache is an atomic
@@ -1885,9 +2011,9 @@ int occupancy16() {  // resident blocks per SM
   int occ = cache.load(std::memory_order_relaxed);
   if (occ < 0) {
 #if AGATHA_MAXNREG16
-    const auto kfn = NREG == 16 ? align16w_kernel<NREG, TRACE, NCAP> : align16_kernel<NREG, TRACE, NCAP>;
+    const auto kfn = NREG == 16 ? align16w_kernel<NREG, TRACE, NCAP, ENDS> : align16_kernel<NREG, TRACE, NCAP, ENDS>;
 #else
-    const auto kfn = align16_kernel<NREG, TRACE, NCAP>;
+    const auto kfn = align16_kernel<NREG, TRACE, NCAP, ENDS>;
 #endif
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 32 * Front16<NREG>::wpb, 0) != cudaSuccess) {
       cudaGetLastError();
@@ -1908,10 +2034,10 @@ long long warp_slots16(const agatha_ctx* ctx, int t) {
 
 // Launch helpers: grid = the persistent grid; *units_out = packing-scratch units the
 // launch uses (warps, or blocks of the wide tier).  dry: size only, launch nothing.
-template <int NREG, bool TRACE, int NCAP>
+template <int NREG, bool TRACE, int NCAP, bool ENDS = false>
 int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int* units_out = nullptr,
                    bool dry = false) {
-  const int occ = occupancy16<NREG, TRACE, NCAP>();
+  const int occ = occupancy16<NREG, TRACE, NCAP, ENDS>();
   const long long want = (long long)ctx->num_sms * occ;
   constexpr int wpb = Front16<NREG>::wpb;
   const long long need = ((long long)A.n_pairs + wpb - 1) / wpb;
@@ -1921,10 +2047,10 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
   if (units_out) *units_out = grid * wpb;
   if (dry) return AGATHA_OK;
 #if AGATHA_MAXNREG16
-  if (NREG == 16) align16w_kernel<NREG, TRACE, NCAP><<<grid, 32 * wpb, 0, st>>>(A);
+  if (NREG == 16) align16w_kernel<NREG, TRACE, NCAP, ENDS><<<grid, 32 * wpb, 0, st>>>(A);
   else
 #endif
-  align16_kernel<NREG, TRACE, NCAP><<<grid, 32 * wpb, 0, st>>>(A);
+  align16_kernel<NREG, TRACE, NCAP, ENDS><<<grid, 32 * wpb, 0, st>>>(A);
   CUDA_TRY(cudaGetLastError());
   return AGATHA_OK;
 }
@@ -1933,13 +2059,14 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
 #ifndef AGATHA_NCAP7
 #define AGATHA_NCAP7 0  // 1: seven capped registers when every off <= 7 (-0.1%)
 #endif
+template <bool ENDS>
 int launch_align16_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int maxoff,
                         int* units_out = nullptr, bool dry = false) {
 #if AGATHA_NCAP7
-  if (maxoff <= 7) return launch_align16<16, false, 7>(ctx, A, st, grid_out, units_out, dry);
+  if (maxoff <= 7) return launch_align16<16, false, 7, ENDS>(ctx, A, st, grid_out, units_out, dry);
 #endif
-  if (maxoff <= 8) return launch_align16<16, false, 8>(ctx, A, st, grid_out, units_out, dry);
-  return launch_align16<16, false, 16>(ctx, A, st, grid_out, units_out, dry);
+  if (maxoff <= 8) return launch_align16<16, false, 8, ENDS>(ctx, A, st, grid_out, units_out, dry);
+  return launch_align16<16, false, 16, ENDS>(ctx, A, st, grid_out, units_out, dry);
 }
 
 template <int W, bool TRACE>
@@ -2109,9 +2236,12 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
       (rc = grow(ctx->ready, 4 * kMaxChunks)))
     return rc;
   agatha_result_t* d_out = out;
+  agatha_ends_t* d_ends = b->ends;
   if (!dev_out) {
-    if ((rc = grow(ctx->results, sizeof(agatha_result_t) * P))) return rc;
+    if ((rc = grow(ctx->results, (sizeof(agatha_result_t) + (b->ends ? sizeof(agatha_ends_t) : 0)) * P)))
+      return rc;
     d_out = (agatha_result_t*)ctx->results.p;
+    if (b->ends) d_ends = (agatha_ends_t*)(d_out + P);
   }
   // scalars: [0] err_flags [1] max_slots [2] queue (tier 0 / one launch) [3] max (-D) mod 16
   // [4..6] pairs per slot tier [7] max (-D) mod 16 of tier 0 [8] [9] queues of tiers 1, 2
@@ -2228,6 +2358,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   A.ready = d_ready; A.err_flags = d_sc; A.nmap = nmap ? 1 : 0;
   A.roff = d_roff; A.qoff = d_qoff; A.order = d_order; A.bad = (const uint8_t*)ctx->bad.p;
   A.out = d_out; A.n_pairs = (uint32_t)P;
+  A.ends = d_ends;
   A.queue = b->queue ? b->queue : d_sc + 2;  // NEXT #1: a counter shared with other GPUs
   A.sysq = b->queue ? 1 : 0;
   A.static_assign = (b->flags & AGATHA_STATIC_ASSIGN) ? 1 : 0;
@@ -2262,6 +2393,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     CUDA_TRY(cudaEventRecord(ctx->cev[1], ctx->copy_stream));
   }
   int grid = 0, units_total = 0;
+  const bool ends = d_ends != nullptr;
   int tiers_launched = 0, slots = 0;
   memset(ctx->stats.tier_pairs, 0, sizeof(ctx->stats.tier_pairs));
   // two passes over the launch selection: the dry one sizes the packing scratch (units of
@@ -2297,9 +2429,15 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
         if (cudaStreamWaitEvent(ts, ctx->tev[0], 0) != cudaSuccess) { rc = AGATHA_ECUDA; break; }
       }
       int g = 0, u = 0;
-      if (t == 0) rc = launch_align16_wide(ctx, At, ts, &g, maxoff16_t0, &u, dry);
-      else if (t == 1) rc = launch_align16<8, false, NCAP8>(ctx, At, ts, &g, &u, dry);
-      else rc = launch_align16<4, false, 3>(ctx, At, ts, &g, &u, dry);
+      if (ends) {  // NEXT #4: the end-score instantiations
+        if (t == 0) rc = launch_align16_wide<true>(ctx, At, ts, &g, maxoff16_t0, &u, dry);
+        else if (t == 1) rc = launch_align16<8, false, NCAP8, true>(ctx, At, ts, &g, &u, dry);
+        else rc = launch_align16<4, false, 3, true>(ctx, At, ts, &g, &u, dry);
+      } else {
+        if (t == 0) rc = launch_align16_wide<false>(ctx, At, ts, &g, maxoff16_t0, &u, dry);
+        else if (t == 1) rc = launch_align16<8, false, NCAP8>(ctx, At, ts, &g, &u, dry);
+        else rc = launch_align16<4, false, 3>(ctx, At, ts, &g, &u, dry);
+      }
       unit_base += u;
       units += u;
       if (t > 0 && !rc && !dry && cudaEventRecord(ctx->tev[t], ts) != cudaSuccess) rc = AGATHA_ECUDA;
@@ -2315,10 +2453,14 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     // off = (-D) mod 16 is at most 8 (prep_kernel's max); else all sixteen
     const int t = tier_of(maxD);
     int* u = &units;
-    if (t == 2) rc = tr ? launch_align16<4, true, 3>(ctx, A, st, &grid, u, dry) : launch_align16<4, false, 3>(ctx, A, st, &grid, u, dry);
+    if (ends) {  // (tracing never asks for end scores)
+      if (t == 2) rc = launch_align16<4, false, 3, true>(ctx, A, st, &grid, u, dry);
+      else if (t == 1) rc = launch_align16<8, false, NCAP8, true>(ctx, A, st, &grid, u, dry);
+      else rc = launch_align16_wide<true>(ctx, A, st, &grid, maxoff16, u, dry);
+    } else if (t == 2) rc = tr ? launch_align16<4, true, 3>(ctx, A, st, &grid, u, dry) : launch_align16<4, false, 3>(ctx, A, st, &grid, u, dry);
     else if (t == 1) rc = tr ? launch_align16<8, true, NCAP8>(ctx, A, st, &grid, u, dry) : launch_align16<8, false, NCAP8>(ctx, A, st, &grid, u, dry);
     else if (tr) rc = launch_align16<16, true, 16>(ctx, A, st, &grid, u, dry);
-    else rc = launch_align16_wide(ctx, A, st, &grid, maxoff16, u, dry);
+    else rc = launch_align16_wide<false>(ctx, A, st, &grid, maxoff16, u, dry);
     tiers_launched = 1;
     ctx->stats.tier_pairs[t] = (int)P;
     slots = 32 >> t;
@@ -2343,8 +2485,11 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   }
   launches += tiers_launched;
   CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
-  if (!dev_out)
+  if (!dev_out) {
     CUDA_TRY(cudaMemcpyAsync(out, d_out, sizeof(agatha_result_t) * P, cudaMemcpyDeviceToHost, st));
+    if (b->ends)
+      CUDA_TRY(cudaMemcpyAsync(b->ends, d_ends, sizeof(agatha_ends_t) * P, cudaMemcpyDeviceToHost, st));
+  }
   CUDA_TRY(cudaEventRecord(ctx->ev[4], st));
   CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars + 14, d_sc, 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -2523,6 +2668,7 @@ int agatha_localmax_trace(agatha_ctx_t* ctx, const agatha_batch_t* batch, const 
   agatha_batch_t b2 = *batch;
   b2.flags |= AGATHA_OUT_DEVICE;
   b2.queue = nullptr;  // the traced pair must run on this context
+  b2.ends = nullptr;
   rc = run_batch(ctx, &b2, params, tout, st, (long long)pair, ts, ti, cap);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(score, ts, 4 * (size_t)cap, cudaMemcpyDeviceToHost, st));

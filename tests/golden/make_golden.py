@@ -64,6 +64,38 @@ VARIANT_CASES = [
 ]
 
 
+# NEXT #4 end scores (reading R19, minimap2's mqe / mte / end score; outside the
+# paper): (R, Q, band_left, band_right, zdrop, stated (mqe, mqe_i, mte, mte_j, end), why).
+# The stated values are derived by hand: R = Q gives 2n at (n, n) on both ends; a single
+# cell is its own end; a pair terminated before any end cell has none; SURVEY B.1's global
+# max of the one-deletion pair sits at (8, 7), the only reference-end cell in its band.
+NO = -(1 << 30)
+ENDS_CASES = [
+    ("ACGT", "ACGT", FULL, FULL, -1, (8, 4, 8, 4, 8), "R = Q: 2n at (n, n) (SPEC.md S:155)"),
+    ("A", "T", FULL, FULL, -1, (-4, 1, -4, 1, -4), "one cell: both ends and the end score (S:168)"),
+    ("AAAA" + "C" * 12, "AAAA" + "G" * 12, 2, 2, 4, (NO, -1, NO, -1, NO),
+     "terminated at c = 11 (S:157) before any end cell (c >= 17)"),
+    ("AAAAAAAAAA", "AAA", 1, 1, -1, (6, 3, NO, -1, NO),
+     "query end at i = 2..4: H(3,3) = 6 > H(4,3) = 2 > H(2,3) = 0; reference end out of band"),
+    ("ACGTTACG", "ACGTACG", 1, 1, -1, (10, 8, 10, 7, 10),
+     "SURVEY B.1: max 10 first reached at (8, 7), the only cell with i = m in the band"),
+]
+
+
+def write_ends():
+    rows = []
+    for R, Q, bl, br, z, stated, cite in ENDS_CASES:
+        _, got = bruteforce.align_ends(R, Q, match=2, mismatch=4, ambig=4, gap_open=4, gap_extend=2,
+                                       band_left=bl, band_right=br, zdrop=z)
+        if tuple(got) != tuple(stated):
+            raise SystemExit(f"brute force {got} disagrees with stated {stated} for {R}/{Q} ({cite})")
+        rows.append("\t".join([R, Q, str(bl), str(br), str(z), ",".join(str(x) for x in got), cite]))
+    hdr = ("# R\tQ\tband_left\tband_right\tzdrop\tends(mqe,mqe_i,mte,mte_j,end_score)\tcitation  (scoring 2/4/4/4/2)\n"
+           "# written by tests/golden/make_golden.py (oracle.bruteforce); each row equals its stated value\n")
+    with open(os.path.join(HERE, "ends.tsv"), "w") as f:
+        f.write(hdr + "\n".join(rows) + "\n")
+
+
 def write_variants():
     rows = []
     for R, Q, bl, br, z, var, stated, cite in VARIANT_CASES:
@@ -96,6 +128,7 @@ def main():
         f.write(hdr + "\n".join(rows) + "\n")
     print(f"wrote {len(rows)} cases")
     write_variants()
+    write_ends()
 
 
 if __name__ == "__main__":

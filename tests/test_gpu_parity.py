@@ -720,3 +720,51 @@ def test_federated_two_processes_shared_queue(gpu_lib, ctx):
     rc, exp, _ = oracle.align_batch(whole, params)
     assert rc == 0
     _check_claims([got[0], got[1]], whole, params, exp)
+
+
+# NEXT #4: minimap2-style end scores (agatha_ends_t, reading R19) from every
+# kernel (16-bit fronts of all slot tiers, 32-bit, wide tier) against the oracle.
+def compare_ends(gpu_lib, ctx, pairs, params, flags=0):
+    got, gends = gpu_lib.align_pairs_ends(ctx, pairs, params, flags=flags)
+    rc, exp, eends, _ = oracle.align_batch_ends(pairs, params)
+    assert rc == 0
+    bad = np.nonzero(got != exp)[0]
+    assert len(bad) == 0, (len(bad), int(bad[0]), got[bad[0]], exp[bad[0]])
+    fields = ["mqe", "mqe_i", "mte", "mte_j", "end_score"]
+    bad = np.nonzero(np.any(np.stack([gends[f] != eends[f] for f in fields]), axis=0))[0]
+    if len(bad):
+        k = int(bad[0])
+        R, Q = pairs.pair(k)
+        raise AssertionError(f"ends: {len(bad)}/{len(got)} differ; pair {k} (m={len(R)}, n={len(Q)}) "
+                             f"gpu={gends[k]} oracle={eends[k]} params={params} flags={flags}")
+    return gends
+
+
+@pytest.mark.parametrize("band", [0, 1, 3, 16, 63, 200, 511])
+def test_ends_random_short_pairs(gpu_lib, ctx, kflags, band):
+    rng = np.random.default_rng(5000 + band)
+    pairs = synth.random_short_pairs(rng, 200, 300)
+    for z in (-1, 0, 9, 40):
+        compare_ends(gpu_lib, ctx, pairs, dict(SCORING, band_left=band, band_right=band, zdrop=z), flags=kflags)
+    compare_ends(gpu_lib, ctx, pairs, dict(SCORING, band_left=band, band_right=band // 2 + 3, zdrop=20,
+                                           variant=7), flags=kflags)
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "LS10"])
+def test_ends_synthetic_configs(gpu_lib, ctx, kflags, name):
+    cfg = synth.CONFIGS[name]
+    n = {"C1": 400, "C3": 24, "LS10": 300}[name]
+    pairs = synth.generate(cfg, 0, n)
+    e = compare_ends(gpu_lib, ctx, pairs, vars(cfg.scoring), flags=kflags)
+    assert (e["mqe"] != gpu_lib.NO_SCORE).sum() > 0
+
+
+def test_ends_wide_tier_and_unbounded(gpu_lib, ctx):
+    pairs = synth.generate(synth.CONFIGS["CW1"], 0, 6)
+    pairs = synth.from_list([(R[:2500], Q[:2400]) for R, Q in (pairs.pair(k) for k in range(6))])
+    for prm in (dict(SCORING, band_left=700, band_right=700, zdrop=400),
+                dict(SCORING, band_left=1500, band_right=1600, zdrop=-1)):
+        compare_ends(gpu_lib, ctx, pairs, prm)
+        assert ctx.stats()["warps_per_pair"] > 1
+    short = synth.random_short_pairs(np.random.default_rng(9), 120, 200)
+    compare_ends(gpu_lib, ctx, short, dict(SCORING, band_left=-1, band_right=-1, zdrop=-1))

@@ -344,3 +344,67 @@ def test_align_batch_rows_equal_align_one_on_c1_slice():
     for k in range(pairs.n_pairs):
         R, Q = pairs.pair(k)
         assert tuple(res[k].tolist()) == tuple(oracle.align_one(R, Q, params)[1]), k
+
+
+# NEXT #4: minimap2-style end scores (reading R19), pinned by brute force path
+# enumeration on random tiny pairs, by hand-derived golden rows and by a closed form.
+def load_ends():
+    rows = []
+    with open(os.path.join(os.path.dirname(__file__), "golden", "ends.tsv")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            R, Q, bl, br, z, exp, cite = line.rstrip("\n").split("\t")
+            rows.append((R, Q, dict(match=2, mismatch=4, ambig=4, gap_open=4, gap_extend=2,
+                                    band_left=int(bl), band_right=int(br), zdrop=int(z)),
+                         tuple(int(x) for x in exp.split(",")), cite))
+    return rows
+
+
+ENDS_GOLDEN = load_ends()
+
+
+@pytest.mark.parametrize("R,Q,params,expected,cite", ENDS_GOLDEN)
+def test_ends_golden(R, Q, params, expected, cite):
+    rc, _, ends = oracle.align_one_ends(R, Q, params)
+    assert rc == 0
+    assert tuple(ends) == expected, cite
+
+
+def test_ends_vs_bruteforce_random_tiny():
+    rng = np.random.default_rng(777)
+    n_end = 0
+    for _ in range(400):
+        m, n = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        R = "".join(rng.choice(list("ACGTN"), m, p=[0.24, 0.24, 0.24, 0.24, 0.04]))
+        Q = "".join(rng.choice(list("ACGTN"), n, p=[0.24, 0.24, 0.24, 0.24, 0.04]))
+        if rng.random() < 0.5:
+            Q = R[:n]
+        p = _rand_params(rng)
+        rc, res, ends = oracle.align_one_ends(R, Q, p)
+        assert rc == 0
+        exp_res, exp_ends = bruteforce.align_ends(R, Q, **p)
+        assert tuple(res) == tuple(exp_res) and tuple(ends) == tuple(exp_ends), (R, Q, p)
+        n_end += ends[4] != oracle.NO_SCORE
+    assert n_end > 100  # the sample reaches (m, n) often
+
+
+def test_ends_closed_form_identical_and_batch_rows():
+    """R = Q, full band, Z off: every end score is a*n at (n, n); batch rows equal single rows."""
+    rng = np.random.default_rng(3)
+    lst = []
+    for L in (1, 2, 7, 33, 150):
+        s = "".join(rng.choice(list("ACGT"), L))
+        lst.append((s, s))
+        rc, res, ends = oracle.align_one_ends(s, s, dict(match=3, band_left=-1, band_right=-1))
+        assert ends == (3 * L, L, 3 * L, L, 3 * L)
+    lst += [("ACGTTACG", "ACGTACG"), ("A" * 30, "A" * 5), ("GATTACA" * 9, "GATACA" * 9)]
+    pairs = synth.from_list(lst)
+    p = dict(match=2, mismatch=4, gap_open=4, gap_extend=2, band_left=3, band_right=5, zdrop=6)
+    rc, res, ends, _ = oracle.align_batch_ends(pairs, p, threads=3)
+    assert rc == 0
+    rc0, res0, _ = oracle.align_batch(pairs, p)
+    assert res.tobytes() == res0.tobytes()  # the records do not depend on the ends output
+    for k, (R, Q) in enumerate(lst):
+        _, r1, e1 = oracle.align_one_ends(R, Q, p)
+        assert tuple(res[k].tolist()) == tuple(r1) and tuple(ends[k].tolist())[:5] == tuple(e1), k
