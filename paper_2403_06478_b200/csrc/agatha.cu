@@ -967,6 +967,7 @@ __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A)
 #ifndef AGATHA_LOOPSLIM
 #define AGATHA_LOOPSLIM 0
 #endif
+
 // Stored half-words live in [kW16, kTop16 + 127].  With AGATHA_POS16 (default) the domain
 // is shifted up by kShift16 into [2495, 31743]: every live half-word is then a positive
 // int16 whose bit pattern is also a finite, normal, positive fp16, and positive fp16 bit
@@ -1229,23 +1230,28 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
 #define HLMAX(a, b) vmax2(a, b)
 #endif
 
+// Hout: the registers of parity PAR written by this step; Hd: the same registers two
+// anti-diagonals back (the diagonal term); Hn: the other parity, one anti-diagonal back
+// (the neighbours).  The loop passes one array three times (each step updates its parity
+// in place); a double-buffered front was measured 32% slower.
 template <int NREG, int NCAP, int PAR, bool MASKED>
-__device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], uint32_t (&F)[NREG],
+__device__ __forceinline__ int step16(uint32_t (&Hout)[NREG], const uint32_t (&Hd)[NREG], const uint32_t (&Hn)[NREG],
+                                      uint32_t (&E)[NREG], uint32_t (&F)[NREG],
                                       const uint32_t (&CAP)[NCAP], const uint32_t (&S2)[NREG / 2],
                                       uint32_t AmB2, int lane, uint32_t V2, uint32_t k65536,
                                       uint32_t one, uint32_t KEEPX, uint32_t LMK) {
   const uint32_t W2 = pack2(kW16, kW16);
   uint32_t xH, xEF;
   if (PAR == 0) {  // register 0: (lane-1's slot K-1, own slot NREG-1) from register NREG-1
-    uint32_t sh = __shfl_up_sync(kFull, H[NREG - 1], 1);
+    uint32_t sh = __shfl_up_sync(kFull, Hn[NREG - 1], 1);
     uint32_t se = __shfl_up_sync(kFull, E[NREG - 1], 1);
     if (lane == 0) { sh = W2; se = W2; }
-    xH = prmt(sh, H[NREG - 1], 0x5432);
+    xH = prmt(sh, Hn[NREG - 1], 0x5432);
     xEF = prmt(se, E[NREG - 1], 0x5432);
   } else {         // register NREG-1: (own slot NREG, lane+1's slot 0) from register 0
-    const uint32_t sh = __shfl_down_sync(kFull, H[0], 1);
+    const uint32_t sh = __shfl_down_sync(kFull, Hn[0], 1);
     const uint32_t sf = __shfl_down_sync(kFull, F[0], 1);
-    xH = (prmt(H[0], sh, 0x5432) & KEEPX) | (W2 & ~KEEPX);
+    xH = (prmt(Hn[0], sh, 0x5432) & KEEPX) | (W2 & ~KEEPX);
     xEF = (prmt(F[0], sf, 0x5432) & KEEPX) | (W2 & ~KEEPX);
   }
   uint32_t lm = W2, prev = W2;
@@ -1253,19 +1259,19 @@ __device__ __forceinline__ int step16(uint32_t (&H)[NREG], uint32_t (&E)[NREG], 
 #pragma unroll
   for (int k = 0; k < NREG / 2; ++k) {
     const int j = PAR + 2 * k;
-    const uint32_t hu = (j == 0) ? xH : H[j - 1];
+    const uint32_t hu = (j == 0) ? xH : Hn[j - 1];
     const uint32_t eu = (j == 0) ? xEF : E[j - 1];
-    const uint32_t hl = (j == NREG - 1) ? xH : H[j + 1];
+    const uint32_t hl = (j == NREG - 1) ? xH : Hn[j + 1];
     const uint32_t fl = (j == NREG - 1) ? xEF : F[j + 1];
     const uint32_t e = vaddmax2(eu, AmB2, hu);                 // Eq. 2 (shifted)
     const uint32_t f = vaddmax2(fl, AmB2, hl);                 // Eq. 3 (shifted)
 #if AGATHA_FMA_ADD
-    uint32_t h = __vimax3_s16x2(add16x2_fma(H[j], S2[k], one), e, f);  // Eq. 1 (shifted)
+    uint32_t h = __vimax3_s16x2(add16x2_fma(Hd[j], S2[k], one), e, f);  // Eq. 1 (shifted)
 #else
-    uint32_t h = vaddmax2(H[j], S2[k], vmax2(e, f));                    // Eq. 1 (shifted)
+    uint32_t h = vaddmax2(Hd[j], S2[k], vmax2(e, f));                    // Eq. 1 (shifted)
 #endif
     if (j < NCAP) h = HCAP(h, CAP[j < NCAP ? j : 0]);          // padding slots stay <= kCapNeg16
-    H[j] = h;
+    Hout[j] = h;
     E[j] = e;
     F[j] = f;
     if (MASKED) {
@@ -1484,7 +1490,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     if (lane == 0) ends_init(erec);
     __syncwarp();
   }
-  auto capture = [&](int c, int P, int Bc) {
+  auto capture = [&](const uint32_t (&H)[NREG], int c, int P, int Bc) {
     const int uc = (c - P + dls) >> 1;
     const int ib = uc + P + lane * NC, jb = uc - dls - lane * NC;
     ends_capture(erec, ib, jb, NC, m, n,
@@ -1535,9 +1541,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         thi = min(m - ib, jb - 1);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, NCAP, 0, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
+      const int lmax = step16<NREG, NCAP, 0, MASKED>(H, H, H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
       const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
-      if (MASKED && ENDS) capture(cb - 1, 1, B_prev);
+      if (MASKED && ENDS) capture(H, cb - 1, 1, B_prev);
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
       if (!AGATHA_STEADYC || MASKED) {
@@ -1567,9 +1573,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         thi = min(m - ib, jb - 1);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, NCAP, 1, MASKED>(H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
+      const int lmax = step16<NREG, NCAP, 1, MASKED>(H, H, H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
       const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
-      if (MASKED && ENDS) capture(cb, 0, B_prev);
+      if (MASKED && ENDS) capture(H, cb, 0, B_prev);
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
       if (!AGATHA_STEADYC || MASKED) {
@@ -1656,7 +1662,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
     run_phase(TrueT{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);  // tail: cb <= c_last
   }
   if (!stop) {
-    if (ENDS) capture(cb - 1, 1, B_prev);
+    if (ENDS) capture(H, cb - 1, 1, B_prev);
     process16<NREG, 1, TRACE, false>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
   }
   if (ENDS && lane == 0) ends_store(A.ends + pid, erec);
