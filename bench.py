@@ -81,6 +81,8 @@ def parse():
     ap.add_argument("--pairs", type=int, default=0, help="pairs per GPU (default: the config's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the Z-drop-heavy side measurement (C3) added to the default C2 line")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample stride (0: auto)")
     ap.add_argument("--order", default="lpt", choices=["lpt", "input"])
     ap.add_argument("--tiers", default="split", choices=["split", "single"],
@@ -625,6 +627,37 @@ def main():
         mism = int((res[idx] != ores).sum())
         parity = {"pairs_checked": int(len(idx)), "mismatches": mism}
 
+    # C2 never triggers Z-drop (p_chim = 0): the default run also times the Z-drop-heavy
+    # C3 batch (50% chimeric; BASELINE.json configs[2]) on the same context, device-resident
+    zdrop_side = None
+    if (not args.no_extra and world == 1 and args.config == "C2" and not dynamic
+            and args.order == "lpt" and args.tiers == "split" and args.refill == "queue"):
+        c3 = synth.CONFIGS["C3"]
+        p3 = synth.generate(c3)
+        prm3 = dict(vars(c3.scoring))
+        d3 = [torch.from_numpy(np.ascontiguousarray(a)).cuda()
+              for a in (p3.ref, p3.ref_off.view(np.int64), p3.qry, p3.qry_off.view(np.int64))]
+        o3 = torch.zeros(adist.RECORD_BYTES * p3.n_pairs, dtype=torch.uint8, device="cuda")
+        agatha.align_batch(ctx, d3[0], d3[1], d3[2], d3[3], prm3, out=o3, stream=stream)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(3):
+            agatha.align_batch(ctx, d3[0], d3[1], d3[2], d3[3], prm3, out=o3, stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        r3 = agatha.device_results(o3)
+        ms3 = ev0.elapsed_time(ev1) / 3
+        zdrop_side = {"config": f"C3: {c3.description}", "pairs": int(p3.n_pairs),
+                      "value": float(r3["cells"].sum()) / (ms3 / 1e3) / 1e9, "unit": "GCUPS",
+                      "ms_per_step": ms3, "steps": 3, "warmup": 1,
+                      "zdrop_terminated": int((r3["zdrop_antidiag"] >= 0).sum())}
+        if not args.no_cpu:
+            idx3 = np.arange(0, p3.n_pairs, 1000)
+            import oracle
+            rc3, e3, _ = oracle.align_batch(p3.subset(idx3), prm3, threads=cpu_cores())
+            zdrop_side["parity"] = {"pairs_checked": int(len(idx3)), "mismatches": int((r3[idx3] != e3).sum())}
+        del d3, o3
+
     par = (f"{world} GPU(s) claim pairs of the federated batch from one shared counter (system-scope "
            "atomics; a stolen pair read from its owner's HBM over NVLink, NEXT #1)"
            if dynamic else (f"LPT partition over nominal cells into {world} shards, NCCL all_gather"
@@ -640,7 +673,7 @@ def main():
                        refill=args.refill),
         "alignments_per_s": aln_s,
         "cells_per_step": cells_all, "zdrop_terminated": int((res["zdrop_antidiag"] >= 0).sum()),
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "zdrop_workload": zdrop_side,
         "paper_speedup": PAPER_SPEEDUP,
         "gpu_launches": launches_all,
         "library_launches": stats["library_launches"] * args.steps * world,
