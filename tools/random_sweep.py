@@ -100,13 +100,19 @@ def main():
         if prm["band_left"] < 0 or prm["band_right"] < 0:
             lst = [(R[:1500], Q[:1500]) for R, Q in lst]  # unbounded: keep the D <= 4096 limit
         pairs = synth.from_list(lst)
-        flags = int(rng.choice([0, 0, 0, agatha.ORDER_INPUT, agatha.SINGLE_TIER, agatha.FORCE_32BIT]))
+        flags = int(rng.choice([0, 0, 0, agatha.ORDER_INPUT, agatha.SINGLE_TIER, agatha.FORCE_32BIT,
+                                agatha.STATIC_ASSIGN]))
+        want_ends = rng.random() < 0.3  # NEXT #4 end scores on some batches
+        gends = None
         try:
-            got = agatha.align_pairs(ctx, pairs, prm, flags=flags)
+            if want_ends:
+                got, gends = agatha.align_pairs_ends(ctx, pairs, prm, flags=flags)
+            else:
+                got = agatha.align_pairs(ctx, pairs, prm, flags=flags)
             rc_gpu = 0
         except agatha.AgathaError as e:
             got, rc_gpu = None, e.code
-        rc, exp, _ = oracle.align_batch(pairs, prm)
+        rc, exp, eends, _ = oracle.align_batch_ends(pairs, prm)
         st = ctx.stats() if got is not None else {}
         line = {"batch": k, "pairs": pairs.n_pairs, "params": prm, "flags": flags, "rc_gpu": rc_gpu,
                 "rc_oracle": rc, "packed16": st.get("packed16"), "tier_pairs": st.get("tier_pairs")}
@@ -117,6 +123,12 @@ def main():
             line["limit_checked"] = True
         else:
             bad = np.nonzero(got != exp)[0]
+            if gends is not None:
+                f5 = ["mqe", "mqe_i", "mte", "mte_j", "end_score"]
+                bad_e = np.nonzero(np.any(np.stack([gends[f] != eends[f] for f in f5]), axis=0))[0]
+                line["ends_checked"] = True
+                line["ends_mismatches"] = int(len(bad_e))
+                bad = np.union1d(bad, bad_e)
             line["mismatches"] = int(len(bad))
             line["ok"] = rc == 0 and len(bad) == 0
             if len(bad):
