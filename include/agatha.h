@@ -36,8 +36,11 @@ extern "C" {
 #define AGATHA_EINVAL (-1) /* invalid scoring parameters or arguments  */
 #define AGATHA_EEMPTY (-2) /* a sequence of length 0 or n_pairs == 0 */
 #define AGATHA_ECHAR (-3)  /* a non-ACGTN byte under AGATHA_N_REJECT         */
-#define AGATHA_ERANGE (-4) /* band wider than 4096 diagonals, penalties > 127, or a pair so
-                              long that |H| could reach 2^20         */
+#define AGATHA_ERANGE (-4) /* band wider than 4096 diagonals, penalties > 127, a pair with
+                              alpha*(m+n) + |H| >= 2^30 or >= 2^31 cells, or (only when the
+                              32-bit kernel must run: scoring outside the 16-bit guard,
+                              bands over 1024 diagonals, AGATHA_FORCE_32BIT) a pair so long
+                              that |H| could reach 2^20            */
 #define AGATHA_ECUDA (-5)  /* CUDA runtime failure / no sm_100a device                    */
 #define AGATHA_ENOMEM (-6) /* device allocation failed                                    */
 

@@ -1835,7 +1835,12 @@ __global__ void prep_kernel(PrepArgs P) {
     // |H| bound: alpha + max(bl,br)*beta + max(a,b,n)*min(m,n)
     const int64_t hb = (int64_t)P.alpha + (bl > br ? bl : br) * (int64_t)P.beta +
                        (int64_t)P.maxs * (m < n ? m : n);
-    if (!flag && (D > kMaxSlotsWide || hb >= kHLimit - 16 || m + n >= (1LL << 30))) flag = 4;
+    // Range: every kernel keeps alpha*c + |H| and a pair's cell count in
+    // int32 (flag 4: ERANGE); only the 32-bit kernels pack H into a 16*H key with per-slot
+    // caps, which needs |H| < 2^20 (flag 8: ERANGE unless the 16-bit kernel runs)
+    if (!flag && (D > kMaxSlotsWide || m + n >= (1LL << 30) ||
+                  (int64_t)P.alpha * (m + n + 2) + hb >= (1LL << 30)))
+      flag = 4;
     // nominal in-band in-table cells: sum over diagonals d of |{i : 1<=i<=m, 1<=i-d<=n}|
     uint64_t cnt = 0;
     if (!flag) {
@@ -1847,6 +1852,8 @@ __global__ void prep_kernel(PrepArgs P) {
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+    if (!flag && cnt >= (1ull << 31)) flag = 4;
+    const bool long32 = !flag && hb >= kHLimit - 16;
     if (lane == 0) {
       const uint32_t nom = (uint32_t)(cnt > 0xffffffffull ? 0xffffffffull : cnt);
       P.nominal[p] = nom;
@@ -1869,6 +1876,7 @@ __global__ void prep_kernel(PrepArgs P) {
         atomicOr(P.err_flags, flag);
         if (P.tier_count) atomicAdd(P.tier_count, 1);  // (the call then fails anyway)
       } else {
+        if (long32) atomicOr(P.err_flags, 8);
         if (P.max_len) {
           atomicMax(P.max_len, (int)m);
           atomicMax(P.max_len + 1, (int)n);
@@ -2301,6 +2309,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
 
   const int K = maxD <= 512 ? 16 : 32;
   const bool k16 = use16(p, maxD) && !(b->flags & AGATHA_FORCE_32BIT);
+  if ((err0 & 8) && !k16) return AGATHA_ERANGE;  // a pair the 32-bit kernels cannot hold
   if (b->queue) {
     // Participants of a shared queue claim positions of ONE order with one counter per
     // launch: they must agree on the batch, the parameters and every choice that shapes

@@ -144,3 +144,24 @@ def test_narrow_bands_long_pairs(gpu_lib, ctx):
     for bl, br, exp16 in [(0, 0, False), (1, 0, True), (0, 1, True), (1, 1, True), (2, 2, True)]:
         both(gpu_lib, ctx, pairs, dict(match=2, mismatch=4, ambig=4, gap_open=4, gap_extend=2,
                                        band_left=bl, band_right=br, zdrop=-1), expect16=exp16)
+
+
+def test_ultra_long_pair(gpu_lib, ctx):
+    """A 300 kbp read (|H| beyond the 32-bit kernels' 2^20 bound) runs on the 16-bit
+    kernel and matches the oracle; the 32-bit kernel refuses it with ERANGE."""
+    rng = np.random.default_rng(31)
+    L = 300_000
+    a = rand_seq(rng, L)
+    q = list(a)
+    for k in range(0, L, 97):  # ~1% substitutions
+        q[k] = "ACGT"[("ACGT".index(q[k]) + 1) % 4]
+    pairs = synth.from_list([(a + rand_seq(rng, 200), "".join(q)), (rand_seq(rng, 5000), rand_seq(rng, 4000))])
+    params = dict(match=2, mismatch=4, ambig=4, gap_open=4, gap_extend=2, band_left=60, band_right=60, zdrop=400)
+    got = gpu_lib.align_pairs(ctx, pairs, params)
+    assert ctx.stats()["packed16"] == 1
+    rc, exp, _ = oracle.align_batch(pairs, params)
+    assert rc == 0 and got.tobytes() == exp.tobytes(), (got, exp)
+    assert got[0]["score"] > (1 << 20) // 2 and got[0]["score"] > 2 * L * 0.9 - 6 * L // 97
+    with pytest.raises(gpu_lib.AgathaError) as ei:
+        gpu_lib.align_pairs(ctx, pairs, params, flags=gpu_lib.FORCE_32BIT)
+    assert ei.value.code == gpu_lib.ERANGE
