@@ -81,6 +81,11 @@ def parse():
     ap.add_argument("--pairs", type=int, default=0, help="pairs per GPU (default: the config's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collective backend (gloo + --same-device: exercise the N-rank path "
+                         "on one GPU, for testing)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank uses cuda:0 (testing the rank logic on a one-GPU box)")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the Z-drop-heavy side measurement (C3) added to the default C2 line")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample stride (0: auto)")
@@ -161,7 +166,7 @@ def launch_ranks(args) -> int:
     import torch
 
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and not args.same_device:
         print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
               file=sys.stderr, flush=True)
         return 2
@@ -344,12 +349,17 @@ def main():
     from paper_2403_06478_b200 import agatha
     from paper_2403_06478_b200 import dist as adist
 
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         # NCCL's init log shows the communicator's rank count (nRanks) to the driver
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     sc = cfg.scoring
     n_cfg = args.pairs or cfg.n_pairs
     n_global = n_cfg * world if args.scaling == "weak" else n_cfg

@@ -128,7 +128,10 @@ def gather_results(local, world: int, group=None):
     if world == 1:
         return local
     out = torch.empty(local.numel() * world, dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(out, local, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, local, group=group)
+    else:  # gloo (CPU tests, or the one-GPU test mode of bench.py): list form
+        dist.all_gather(list(out.chunk(world)), local, group=group)
     return out
 
 
