@@ -209,3 +209,21 @@ def test_bench_refuses_more_gpus_than_visible():
     assert r.returncode == 2, (r.returncode, r.stdout[-500:], r.stderr[-500:])
     assert "needs 2 visible GPUs" in r.stderr
     assert not r.stdout.strip()  # no JSON line claiming a 1-GPU result
+
+
+def test_bench_reference_arm_line():
+    """`bench.py --impl reference` (the oracle on the host cores, this tier's reference arm)
+    prints one JSON line with the contract's keys; no GPU involved."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--config", "C1",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-1000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["metric"] == "GCUPS" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["higher_is_better"] is True and d["config"]["workload"].startswith("C1")
