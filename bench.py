@@ -471,6 +471,7 @@ def main():
     stats = ctx.stats()
     res = agatha.device_results(d_out)
     ms_max = adist.max_over_ranks(ms, "cuda", world)
+    ms_mean = adist.sum_over_ranks(ms, "cuda", world) / world  # imbalance = max / mean
     if dynamic:  # res is the merged federated batch; this rank aligned the pairs it claimed
         cells_all = float(res["cells"].sum())
         cells_rank = int(state["mine"].item())
@@ -693,6 +694,8 @@ def main():
     }
     if world > 1:
         line["rank0_pairs"] = n_local
+        line["rank_time"] = {"max_ms_per_step": ms_max / args.steps, "mean_ms_per_step": ms_mean / args.steps,
+                             "imbalance": ms_max / ms_mean if ms_mean > 0 else None}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
