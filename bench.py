@@ -458,16 +458,19 @@ def main():
     barrier()
     align_ms = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
         state["launches"] = 0
-        for _ in range(args.steps):
+        for k in range(args.steps):
             step()
+            step_ev[k].record(stream)  # per-step boundaries (median and min)
             align_ms.append(state["kernel_ms"])
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
+    step_ms = [ev0.elapsed_time(step_ev[0])] + [step_ev[k - 1].elapsed_time(step_ev[k]) for k in range(1, args.steps)]
     stats = ctx.stats()
     res = agatha.device_results(d_out)
     ms_max = adist.max_over_ranks(ms, "cuda", world)
@@ -684,6 +687,8 @@ def main():
                        parallelism=par, scaling=args.scaling, order=args.order, tiers=args.tiers,
                        refill=args.refill),
         "alignments_per_s": aln_s,
+        "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms),
+                    "note": "rank 0's per-step device times; value uses the total over all steps"},
         "cells_per_step": cells_all, "zdrop_terminated": int((res["zdrop_antidiag"] >= 0).sum()),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "zdrop_workload": zdrop_side,
         "paper_speedup": PAPER_SPEEDUP,
