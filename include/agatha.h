@@ -159,6 +159,8 @@ typedef struct {
   int32_t input_chunks;  /* host inputs: chunks streamed under the kernel (1 for device)  */
   int32_t lpt_from_chunk; /* chunks from this one on are dispatched as one longest-first
                              group (they arrive before the queue reaches them)           */
+  int32_t pin_off;     /* 32-slot front: the common low padding off = (-D) mod 16 of its
+                          pairs when the pinned front ran (one capped slot), else -1     */
 } agatha_stats_t;
 
 /* Create a context on CUDA device `cuda_device`.  Fails with AGATHA_ECUDA when the

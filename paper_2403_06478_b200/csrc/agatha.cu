@@ -1234,10 +1234,24 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
 // anti-diagonals back (the diagonal term); Hn: the other parity, one anti-diagonal back
 // (the neighbours).  The loop passes one array three times (each step updates its parity
 // in place); a double-buffered front was measured 32% slower.
+// Padding below the band (DESIGN.md §6.1 "Layout"): NCAP < 100 caps registers 0..NCAP-1
+// every step (any off <= NCAP); NCAP = 100 + off ("pinned", every pair of the launch has
+// this off) caps only slot off-1, the one padding slot a band cell reads: its H, E and F
+// every step, and the dead slots under it only at each re-centring (their growth between
+// re-centrings is bounded on the host, pin16_ok), so they stay below kEmpty16.
+template <int NCAP> struct CapMode {
+  static constexpr bool pin = NCAP >= 100;
+  static constexpr int off = pin ? NCAP - 100 : 0;
+  static constexpr int ncap = pin ? 1 : NCAP;  // cap words held
+};
+#ifndef AGATHA_REDUX2
+#define AGATHA_REDUX2 0  // 1: warp max of both halves as two REDUX (no VIMNMX half merge)
+#endif
+
 template <int NREG, int NCAP, int PAR, bool MASKED>
-__device__ __forceinline__ int step16(uint32_t (&Hout)[NREG], const uint32_t (&Hd)[NREG], const uint32_t (&Hn)[NREG],
+__device__ __forceinline__ uint32_t step16(uint32_t (&Hout)[NREG], const uint32_t (&Hd)[NREG], const uint32_t (&Hn)[NREG],
                                       uint32_t (&E)[NREG], uint32_t (&F)[NREG],
-                                      const uint32_t (&CAP)[NCAP], const uint32_t (&S2)[NREG / 2],
+                                      const uint32_t (&CAP)[CapMode<NCAP>::ncap], const uint32_t (&S2)[NREG / 2],
                                       uint32_t AmB2, int lane, uint32_t V2, uint32_t k65536,
                                       uint32_t one, uint32_t KEEPX, uint32_t LMK) {
   const uint32_t W2 = pack2(kW16, kW16);
@@ -1263,14 +1277,22 @@ __device__ __forceinline__ int step16(uint32_t (&Hout)[NREG], const uint32_t (&H
     const uint32_t eu = (j == 0) ? xEF : E[j - 1];
     const uint32_t hl = (j == NREG - 1) ? xH : Hn[j + 1];
     const uint32_t fl = (j == NREG - 1) ? xEF : F[j + 1];
-    const uint32_t e = vaddmax2(eu, AmB2, hu);                 // Eq. 2 (shifted)
-    const uint32_t f = vaddmax2(fl, AmB2, hl);                 // Eq. 3 (shifted)
+    uint32_t e = vaddmax2(eu, AmB2, hu);                       // Eq. 2 (shifted)
+    uint32_t f = vaddmax2(fl, AmB2, hl);                       // Eq. 3 (shifted)
 #if AGATHA_FMA_ADD
     uint32_t h = __vimax3_s16x2(add16x2_fma(Hd[j], S2[k], one), e, f);  // Eq. 1 (shifted)
 #else
     uint32_t h = vaddmax2(Hd[j], S2[k], vmax2(e, f));                    // Eq. 1 (shifted)
 #endif
-    if (j < NCAP) h = HCAP(h, CAP[j < NCAP ? j : 0]);          // padding slots stay <= kCapNeg16
+    if (CapMode<NCAP>::pin) {
+      if (j == CapMode<NCAP>::off - 1) {  // slot off-1 (lane 0): the only padding a band cell reads
+        h = vmin2(h, CAP[0]);
+        e = vmin2(e, CAP[0]);
+        f = vmin2(f, CAP[0]);
+      }
+    } else if (j < NCAP) {
+      h = HCAP(h, CAP[j < NCAP ? j : 0]);                      // padding slots stay <= kCapNeg16
+    }
     Hout[j] = h;
     E[j] = e;
     F[j] = f;
@@ -1294,15 +1316,26 @@ __device__ __forceinline__ int step16(uint32_t (&Hout)[NREG], const uint32_t (&H
   // max of the two halves as an int32: hi16_fma gives (sign(hi) = -1 : hi), and every
   // H half is negative (<= kTop16), so the pair max is (-1 : max(lo, hi)), which read as
   // an int32 is exactly max(lo, hi)
+  if (AGATHA_REDUX2) return lm;  // warp_max16 reduces both halves
 #if AGATHA_LMSHL
   // (lm << 16 as a full-rate IMAD): the high half becomes max(hi, lo) and the low half
   // max(lo, 0) (= 0 for negative halves, lo for AGATHA_POS16), so the high half of the
   // lane value is max(lo, hi) and the warp max is recovered by one uniform arithmetic
   // shift after the REDUX (LANEMAX16); the low half only breaks ties between lanes
-  return (int)HLMAX(lm, lm * k65536);
+  return HLMAX(lm, lm * k65536);
 #else
-  return (int)vmax2(lm, (uint32_t)hi16_fma(lm, k65536));
+  return vmax2(lm, (uint32_t)hi16_fma(lm, k65536));
 #endif
+}
+
+// Warp max (Eq. 5) of one step's lane value (step16's return)
+__device__ __forceinline__ int warp_max16(uint32_t lv, uint32_t k65536) {
+  if (AGATHA_REDUX2) {  // lv = the masked lane max pair: one REDUX per half
+    const int a = __reduce_max_sync(kFull, (int)lv);              // max hi (ties by lo)
+    const int b = __reduce_max_sync(kFull, (int)(lv * k65536));   // max lo
+    return (a > b ? a : b) >> 16;
+  }
+  return LANEMAX16(__reduce_max_sync(kFull, (int)lv));
 }
 
 template <int NREG, bool TRACE, int NCAP, bool ENDS = false>
@@ -1382,7 +1415,7 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   // parity(cb) holds anti-diagonal cb-2, the other parity cb-1 (both <= 0).  Slots start
   // at bnd(d) + alpha*c (stored units), diagonal 0 at the origin value 0, E/F at -inf;
   // DESIGN.md §6.2 "Masking" shows these reproduce the boundary exactly.
-  uint32_t H[NREG], E[NREG], F[NREG], CAP[NCAP];
+  uint32_t H[NREG], E[NREG], F[NREG], CAP[CapMode<NCAP>::ncap];
   const uint32_t W2 = pack2(kW16, kW16);
 #pragma unroll
   for (int j = 0; j < NREG; ++j) {
@@ -1396,10 +1429,11 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
       v2[h] = valid ? (d == 0 ? 0 : bnd(d) + alpha * ci) - s.B : kCapNeg16;
     }
     H[j] = pack2(v2[0], v2[1]);
-    if (j < NCAP) CAP[j < NCAP ? j : 0] = pack2(c2[0], c2[1]);
+    if (!CapMode<NCAP>::pin && j < NCAP) CAP[j < NCAP ? j : 0] = pack2(c2[0], c2[1]);
     E[j] = W2;
     F[j] = W2;
   }
+  if (CapMode<NCAP>::pin) CAP[0] = pack2(lane == 0 ? kCapNeg16 : 0x7FFF, 0x7FFF);
 
   int rpos = u - 1 + padR + lane * NC;
   int wR = rpos >> 3, oR = rpos & 7;  // oR = 0
@@ -1541,8 +1575,8 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         thi = min(m - ib, jb - 1);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, NCAP, 0, MASKED>(H, H, H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
-      const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
+      const uint32_t lmax = step16<NREG, NCAP, 0, MASKED>(H, H, H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
+      const int rH = warp_max16(lmax, k65536);
       if (MASKED && ENDS) capture(H, cb - 1, 1, B_prev);
       if (process16<NREG, 1, TRACE, !MASKED>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -1573,8 +1607,8 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
         thi = min(m - ib, jb - 1);
         V2 = valid_bits(tlo, thi);
       }
-      const int lmax = step16<NREG, NCAP, 1, MASKED>(H, H, H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
-      const int rH = LANEMAX16(__reduce_max_sync(kFull, lmax));
+      const uint32_t lmax = step16<NREG, NCAP, 1, MASKED>(H, H, H, E, F, CAP, S2, AmB2, lane, V2, k65536, one, KEEPX, LMK);
+      const int rH = warp_max16(lmax, k65536);
       if (MASKED && ENDS) capture(H, cb, 0, B_prev);
       if (process16<NREG, 0, TRACE, !MASKED>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
       rH_prev = rH;
@@ -1626,6 +1660,16 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
           }
         }
         s.B += delta;
+      }
+      if (CapMode<NCAP>::pin) {  // (after the shift) re-pin the dead padding slots under slot off-1
+#pragma unroll
+        for (int j = 0; j < CapMode<NCAP>::off - 1; ++j) {
+          H[j] = vmin2(H[j], CAP[0]);
+          if (j & 1) {  // E/F of the last step's parity are the live ones
+            E[j] = vmin2(E[j], CAP[0]);
+            F[j] = vmin2(F[j], CAP[0]);
+          }
+        }
       }
     }
   };
@@ -1798,6 +1842,7 @@ struct PrepArgs {
                                 // range): the queue reaches them after they have arrived
   int* tier_count;              // [3] pairs per slot tier (tier_of)
   int* max_off16_t0;            // max (-D) mod 16 over the pairs of tier 0
+  int* off_mask16;              // [2] OR of 1 << ((-D) mod 16) over the batch / its tier 0
   unsigned long long* len_hash; // shared queue (NEXT #1): sum over pairs of a hash of
                                 // (p, m, n), the batch part of the queue fingerprint
 };
@@ -1883,9 +1928,13 @@ __global__ void prep_kernel(PrepArgs P) {
         }
         atomicMax(P.max_slots, (int)D);
         atomicMax(P.max_off16, (int)((-D) & 15));
+        if (P.off_mask16) atomicOr(P.off_mask16, 1 << ((-D) & 15));
         if (P.tier_count) {
           atomicAdd(P.tier_count + tier_of(D), 1);
-          if (tier_of(D) == 0) atomicMax(P.max_off16_t0, (int)((-D) & 15));
+          if (tier_of(D) == 0) {
+            atomicMax(P.max_off16_t0, (int)((-D) & 15));
+            if (P.off_mask16) atomicOr(P.off_mask16 + 1, 1 << ((-D) & 15));
+          }
         }
       }
     }
@@ -1992,6 +2041,18 @@ static int ref16_of(const agatha_params_t* p, int maxD) {
   const long long mx = std::max<long long>(a, std::max<long long>(p->mismatch, p->ambig));
   return (int)(kTop16 - 127 - (drift16(p) + 3 * al + 2 * a + mx + (al - be) * ((long long)maxD + 2)));
 }
+// Pinned fronts (CapMode): between two re-centrings (kRebase16 iterations) the dead
+// padding slots, pinned at kCapNeg16 at the last one, rise by at most kRebase16 times
+// max(S + 2 alpha, 2 (alpha - beta)) in stored units (a diagonal move every two
+// anti-diagonals, or a gap extension every one); they must stay below kEmpty16.
+static bool pin16_ok(const agatha_params_t* p) {
+  const long long al = p->gap_open, be = p->gap_extend;
+  const long long mx = std::max<long long>(p->match, std::max<long long>(-p->mismatch, -p->ambig)) + 2 * al;
+  const long long g = std::max<long long>(mx, 2 * (al - be));
+  return (kRebase16 + 1) * g + 2 * g < kEmpty16 - kCapNeg16;
+}
+// the common off = (-D) mod 16 of a launch's pairs, or -1 when they differ
+static int pin_off(int mask) { return (mask != 0 && (mask & (mask - 1)) == 0) ? __builtin_ctz(mask) : -1; }
 bool use16(const agatha_params_t* p, int maxD) {
   const long long a = p->match, al = p->gap_open, be = p->gap_extend;
   const long long mx = std::max<long long>(a, std::max<long long>(p->mismatch, p->ambig));
@@ -2073,9 +2134,22 @@ int launch_align16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* gr
 #ifndef AGATHA_NCAP7
 #define AGATHA_NCAP7 0  // 1: seven capped registers when every off <= 7 (-0.1%)
 #endif
+#ifndef AGATHA_PIN
+#define AGATHA_PIN 1  // 0: always the capped fronts
+#endif
+template <int OFF>
+int launch_pin16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int* units_out, bool dry,
+                 int off) {
+  if constexpr (OFF < 16) {
+    if (off == OFF) return launch_align16<16, false, 100 + OFF>(ctx, A, st, grid_out, units_out, dry);
+    return launch_pin16<OFF + 1>(ctx, A, st, grid_out, units_out, dry, off);
+  }
+  return AGATHA_EINVAL;
+}
 template <bool ENDS>
 int launch_align16_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int maxoff,
-                        int* units_out = nullptr, bool dry = false) {
+                        int* units_out = nullptr, bool dry = false, int pin = -1) {
+  if (AGATHA_PIN && !ENDS && pin >= 0) return launch_pin16<0>(ctx, A, st, grid_out, units_out, dry, pin);
 #if AGATHA_NCAP7
   if (maxoff <= 7) return launch_align16<16, false, 7, ENDS>(ctx, A, st, grid_out, units_out, dry);
 #endif
@@ -2283,6 +2357,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   int chunk_bits = 0;
   while ((1 << chunk_bits) < nchunks) ++chunk_bits;
   pa.tier_shift = 32 + chunk_bits; pa.tier_count = d_sc + 4; pa.max_off16_t0 = d_sc + 7;
+  pa.off_mask16 = d_sc + 10;
   pa.lpt_from = lpt_from;
   pa.len_hash = b->queue ? (unsigned long long*)(d_sc + 12) : nullptr;  // zeroed with d_sc
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
@@ -2296,6 +2371,10 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   const int err0 = ctx->h_scalars[0], maxD = ctx->h_scalars[1], maxoff16 = ctx->h_scalars[3];
   const int tier_n[3] = {ctx->h_scalars[4], ctx->h_scalars[5], ctx->h_scalars[6]};
   const int maxoff16_t0 = ctx->h_scalars[7];
+  // the pinned 32-slot front (CapMode) when every pair of the launch has one off
+  const int pin_all = pin16_ok(p) ? pin_off(ctx->h_scalars[10]) : -1;
+  ctx->stats.pin_off = -1;
+  const int pin_t0 = pin16_ok(p) ? pin_off(ctx->h_scalars[11]) : -1;
   const int max_m = ctx->h_scalars[16], max_n = ctx->h_scalars[17];
   if (dev_in) {
     tot_r = h_tot[0];
@@ -2449,7 +2528,10 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
         else if (t == 1) rc = launch_align16<8, false, NCAP8, true>(ctx, At, ts, &g, &u, dry);
         else rc = launch_align16<4, false, 3, true>(ctx, At, ts, &g, &u, dry);
       } else {
-        if (t == 0) rc = launch_align16_wide<false>(ctx, At, ts, &g, maxoff16_t0, &u, dry);
+        if (t == 0) {
+          rc = launch_align16_wide<false>(ctx, At, ts, &g, maxoff16_t0, &u, dry, pin_t0);
+          ctx->stats.pin_off = AGATHA_PIN ? pin_t0 : -1;
+        }
         else if (t == 1) rc = launch_align16<8, false, NCAP8>(ctx, At, ts, &g, &u, dry);
         else rc = launch_align16<4, false, 3>(ctx, At, ts, &g, &u, dry);
       }
@@ -2475,7 +2557,10 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
     } else if (t == 2) rc = tr ? launch_align16<4, true, 3>(ctx, A, st, &grid, u, dry) : launch_align16<4, false, 3>(ctx, A, st, &grid, u, dry);
     else if (t == 1) rc = tr ? launch_align16<8, true, NCAP8>(ctx, A, st, &grid, u, dry) : launch_align16<8, false, NCAP8>(ctx, A, st, &grid, u, dry);
     else if (tr) rc = launch_align16<16, true, 16>(ctx, A, st, &grid, u, dry);
-    else rc = launch_align16_wide<false>(ctx, A, st, &grid, maxoff16, u, dry);
+    else {
+      rc = launch_align16_wide<false>(ctx, A, st, &grid, maxoff16, u, dry, pin_all);
+      ctx->stats.pin_off = AGATHA_PIN ? pin_all : -1;
+    }
     tiers_launched = 1;
     ctx->stats.tier_pairs[t] = (int)P;
     slots = 32 >> t;
@@ -2741,6 +2826,7 @@ int agatha_plan(agatha_ctx_t* ctx, const agatha_batch_t* b, const agatha_params_
   pa.bad = (uint8_t*)ctx->bad.p; pa.err_flags = d_sc; pa.max_slots = d_sc + 1; pa.max_off16 = d_sc + 3;
   pa.chunk_first = nullptr; pa.nchunks = 1; pa.chunk_of = nullptr; pa.key64 = nullptr;
   pa.tier_shift = 32; pa.tier_count = nullptr; pa.max_off16_t0 = nullptr; pa.lpt_from = 1;
+  pa.off_mask16 = nullptr;
   pa.len_hash = nullptr; pa.own.n_owners = 0; pa.max_len = nullptr;
   const int prep_blocks = (int)(((P + 7) / 8) < 4096 ? ((P + 7) / 8) : 4096);
   prep_kernel<<<prep_blocks, 256, 0, st>>>(pa);

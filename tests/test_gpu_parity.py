@@ -91,6 +91,63 @@ def test_band_layouts_long_pairs(gpu_lib, ctx, bl, br):
         assert ctx.stats()["packed16"] == 1
 
 
+def _pin_stress_pairs(rng, bl, br, n_pairs=24):
+    """Pairs for the pinned 32-slot front: half of them carry their true alignment on a
+    diagonal just under the band (the dead padding slots see long match runs while the
+    band cells mismatch: the fastest rise of the dead slots against the band, DESIGN.md
+    §6.1 "Layout"), the rest are 3%-error pairs with indels, some with chimeric tails."""
+    lst = []
+    for k in range(n_pairs):
+        m = int(rng.integers(1500, 2600))
+        a = "".join("ACGT"[x] for x in rng.integers(0, 4, m))
+        if k % 2 == 0:  # Q = R shifted: matches on diagonal d = i - j = -(bl + s), under the band
+            s = int(rng.integers(1, 5))
+            q = "".join("ACGT"[x] for x in rng.integers(0, 4, bl + s)) + a
+        else:
+            q = "".join(c if rng.random() > 0.03 else "ACGT"[int(rng.integers(0, 4))] for c in a)
+            if k % 4 == 1:
+                x = int(rng.integers(100, 600))
+                q = q[:x] + q[x + int(rng.integers(5, 80)):]
+            if k % 8 == 3:  # chimeric tail (Z-drop)
+                cut = int(rng.integers(len(q) // 3, len(q)))
+                q = q[:cut] + "".join("ACGT"[x] for x in rng.integers(0, 4, len(q) - cut))
+        lst.append((a, q[: max(bl + br + 2, len(q) - int(rng.integers(0, 50)))]))
+    return lst
+
+
+@pytest.mark.parametrize("off", list(range(16)))
+def test_pinned_front_every_offset(gpu_lib, ctx, off):
+    """The pinned 32-slot front (one capped padding slot, the dead ones re-pinned at each
+    re-centring) at every low padding off = (-D) mod 16: bit-exact with
+    the oracle, with and without Z-drop, and the stats name the front that ran."""
+    D = 1024 - off
+    bl = (D - 1) // 2
+    br = D - 1 - bl
+    rng = np.random.default_rng(9100 + off)
+    pairs = synth.from_list(_pin_stress_pairs(rng, bl, br))
+    for z in (-1, 60):
+        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=bl, band_right=br, zdrop=z))
+        st = ctx.stats()
+        assert st["packed16"] == 1 and st["tier_pairs"][0] == pairs.n_pairs and st["pin_off"] == off, st
+
+
+def test_pinned_front_fast_rising_padding(gpu_lib, ctx):
+    """Scoring with about the largest S + 2 alpha the 16-bit guard admits at D = 1001 (23) under a
+    band whose padding diagonals match everywhere (the dead slots' fastest rise): the
+    pinned front still matches the oracle; a mixed-off batch runs the capped front."""
+    rng = np.random.default_rng(9200)
+    lst = _pin_stress_pairs(rng, 500, 500, 16)
+    pairs = synth.from_list(lst)
+    for sc in (dict(match=1, mismatch=1, ambig=1, gap_open=11, gap_extend=2),
+               dict(match=2, mismatch=4, ambig=4, gap_open=8, gap_extend=1)):
+        compare(gpu_lib, ctx, pairs, dict(sc, band_left=500, band_right=500, zdrop=-1))
+        st = ctx.stats()
+        assert st["packed16"] == 1 and st["pin_off"] == 7, (sc, st)
+    mixed = synth.from_list(lst[:8] + [(a, q[:400 + 7 * k]) for k, (a, q) in enumerate(lst[8:])])
+    compare(gpu_lib, ctx, mixed, dict(SCORING, band_left=500, band_right=500, zdrop=100))
+    assert ctx.stats()["pin_off"] == -1
+
+
 def test_asymmetric_bands_and_penalties(gpu_lib, ctx, kflags):
     rng = np.random.default_rng(77)
     pairs = synth.random_short_pairs(rng, 200, 300)
