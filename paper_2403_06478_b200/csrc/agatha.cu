@@ -1078,6 +1078,39 @@ __device__ __forceinline__ int argmax_diag16(int first, int P, int dlo) {
   return dlo + ls * (2 * NREG) + slot;
 }
 
+// Split layout (align_pair16s): low halves hold slots lane*NREG + j of
+// the first 32*NREG slots, high halves the same of the next 32*NREG, so the cell of a
+// high half lies HV = 16*NREG positions further along the anti-diagonal than its low
+// half.  Cells are numbered t = k (low) and t = HV + k (high) for the [tlo, thi] range.
+// The smallest d (smallest i) holding v: the lowest lane with a low-half candidate, else
+// the lowest lane with a high-half candidate.
+template <int NREG>
+__device__ __forceinline__ int argmax_diag16s(const uint32_t (&r)[NREG / 2], int v, int tlo, int thi, int P,
+                                              int dls) {
+  constexpr int HS = 32 * NREG, HV = HS / 2;
+  int flo = 99, fhi = 99;
+#pragma unroll
+  for (int k = NREG / 2 - 1; k >= 0; --k) {
+    if (lo16(r[k]) == v && k >= tlo && k <= thi) flo = k;
+    if (hi16(r[k]) == v && HV + k >= tlo && HV + k <= thi) fhi = k;
+  }
+  unsigned bal = __ballot_sync(kFull, flo < 99);
+  int half = 0, first = flo;
+  if (bal == 0u) {
+    bal = __ballot_sync(kFull, fhi < 99);
+    half = 1;
+    first = fhi;
+  }
+  const int ls = __ffs(bal) - 1;
+  const int tt = __shfl_sync(kFull, first, ls);
+  return dls + half * HS + ls * NREG + P + 2 * tt;
+}
+template <int NREG, bool SPLIT>
+__device__ __forceinline__ int argmax16(const uint32_t (&r)[NREG / 2], int v, int tlo, int thi, int P, int dls) {
+  if (SPLIT) return argmax_diag16s<NREG>(r, v, tlo, thi, P, dls);
+  return argmax_diag16<NREG>(first_slot16<NREG>(r, v, tlo, thi), P, dls);
+}
+
 // Word of the deferred-argmax snapshot holding register k (of one parity) of `lane`.
 template <int NREG>
 __device__ __forceinline__ int snap_word(int k, int lane) {
@@ -1101,7 +1134,7 @@ __device__ __forceinline__ void store_snapshot(uint32_t* snap, const uint32_t (&
   }
 }
 
-template <int NREG>
+template <int NREG, bool SPLIT = false>
 __device__ __forceinline__ void resolve_G16(State16& s, const uint32_t* snap, int lane) {
   int par, tlo, thi;
   if (AGATHA_SNAPSLIM) {
@@ -1111,7 +1144,8 @@ __device__ __forceinline__ void resolve_G16(State16& s, const uint32_t* snap, in
     const int c = s.G_c;
     par = (c - s.dlo) & 1;
     const int u = (c - par + s.dlo) >> 1;
-    const int ib = u + par + lane * NREG, jb = u - s.dlo - lane * NREG;
+    constexpr int LC = SPLIT ? NREG / 2 : NREG;  // positions per lane along the anti-diagonal
+    const int ib = u + par + lane * LC, jb = u - s.dlo - lane * LC;
     tlo = max(1 - ib, jb - s.n);
     thi = min(s.m - ib, jb - 1);
     s.posC = c;
@@ -1125,7 +1159,7 @@ __device__ __forceinline__ void resolve_G16(State16& s, const uint32_t* snap, in
 #pragma unroll
   for (int k = 0; k < NREG / 2; ++k) r[k] = snap[snap_word<NREG>(k, lane)];
   const int v = s.G_H + s.alpha * s.G_c - s.snapB;
-  const int d = argmax_diag16<NREG>(first_slot16<NREG>(r, v, tlo, thi), par, s.dlo);
+  const int d = argmax16<NREG, SPLIT>(r, v, tlo, thi, par, s.dlo);
   s.G_d = d;
   s.G_i = (s.G_c + d) >> 1;
   s.G_j = s.G_c - s.G_i;
@@ -1136,7 +1170,7 @@ __device__ __forceinline__ void resolve_G16(State16& s, const uint32_t* snap, in
 // still intact (relative to the current base s.B); rH is the warp max relative to Bc.
 // Fast path: three compares and one vote; the argmax work runs only when the global max
 // moves (deferred snapshot) or when Eq. 4 could fire.
-template <int NREG, int PARC, bool TRACE, bool STEADY>
+template <int NREG, int PARC, bool TRACE, bool STEADY, bool SPLIT = false>
 __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c, int rH, int Bc,
                                           int tlo, int thi, const uint32_t (&H)[NREG], int lane,
                                           uint32_t* snap, long long pid) {
@@ -1158,14 +1192,14 @@ __device__ __forceinline__ bool process16(State16& s, const AlignArgs& A, int c,
     uint32_t r[NREG / 2];
 #pragma unroll
     for (int k = 0; k < NREG / 2; ++k) r[k] = H[PARC + 2 * k];
-    const int d = argmax_diag16<NREG>(first_slot16<NREG>(r, Hs + s.alpha * c - s.B, tlo, thi), PARC, s.dlo);
+    const int d = argmax16<NREG, SPLIT>(r, Hs + s.alpha * c - s.B, tlo, thi, PARC, s.dlo);
     const int i = (c + d) >> 1, j = c - i;
     if (TRACE && pid == A.trace_pair && lane == 0 && c < A.trace_cap) {
       A.trace_score[c] = Hs;
       A.trace_i[c] = i;
     }
     if (chk) {
-      resolve_G16<NREG>(s, snap, lane);
+      resolve_G16<NREG, SPLIT>(s, snap, lane);
       const bool gated = (A.variant & AGATHA_VAR_GATE_GE) ? (s.G_i <= i && s.G_j <= j)
                                                            : (s.G_i < i && s.G_j < j);
       if (gated) {
@@ -1248,15 +1282,31 @@ template <int NCAP> struct CapMode {
 #define AGATHA_REDUX2 0  // 1: warp max of both halves as two REDUX (no VIMNMX half merge)
 #endif
 
-template <int NREG, int NCAP, int PAR, bool MASKED>
+template <int NREG, int NCAP, int PAR, bool MASKED, bool SPLIT = false>
 __device__ __forceinline__ uint32_t step16(uint32_t (&Hout)[NREG], const uint32_t (&Hd)[NREG], const uint32_t (&Hn)[NREG],
                                       uint32_t (&E)[NREG], uint32_t (&F)[NREG],
                                       const uint32_t (&CAP)[CapMode<NCAP>::ncap], const uint32_t (&S2)[NREG / 2],
                                       uint32_t AmB2, int lane, uint32_t V2, uint32_t k65536,
-                                      uint32_t one, uint32_t KEEPX, uint32_t LMK) {
+                                      uint32_t one, uint32_t KEEPX, uint32_t LMK, uint32_t SEL0 = 0u) {
   const uint32_t W2 = pack2(kW16, kW16);
   uint32_t xH, xEF;
-  if (PAR == 0) {  // register 0: (lane-1's slot K-1, own slot NREG-1) from register NREG-1
+  if (SPLIT) {
+    // split layout: register 0's up neighbours are lane-1's register NREG-1 (both halves;
+    // lane 0: the wall and lane 31's low half), register NREG-1's left neighbours are
+    // lane+1's register 0 (lane 31: lane 0's high half and the wall); the walls of the
+    // band come in through the per-lane byte selectors SEL0 / KEEPX (= SEL1)
+    if (PAR == 0) {
+      const uint32_t vh = __shfl_sync(kFull, Hn[NREG - 1], (lane + 31) & 31);
+      const uint32_t ve = __shfl_sync(kFull, E[NREG - 1], (lane + 31) & 31);
+      xH = prmt(vh, W2, SEL0);
+      xEF = prmt(ve, W2, SEL0);
+    } else {
+      const uint32_t vh = __shfl_sync(kFull, Hn[0], (lane + 1) & 31);
+      const uint32_t vf = __shfl_sync(kFull, F[0], (lane + 1) & 31);
+      xH = prmt(vh, W2, KEEPX);
+      xEF = prmt(vf, W2, KEEPX);
+    }
+  } else if (PAR == 0) {  // register 0: (lane-1's slot K-1, own slot NREG-1) from register NREG-1
     uint32_t sh = __shfl_up_sync(kFull, Hn[NREG - 1], 1);
     uint32_t se = __shfl_up_sync(kFull, E[NREG - 1], 1);
     if (lane == 0) { sh = W2; se = W2; }
@@ -1736,6 +1786,488 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
   }
 }
 
+#ifndef AGATHA_SPLIT16
+#define AGATHA_SPLIT16 1  // 0: the 32-slot front keeps the paired (j, j + NREG) layout
+#endif
+#ifndef AGATHA_SPLITWIN
+#define AGATHA_SPLITWIN 1  // split front: 1 register windows fed from the streams, 0 smem rows
+#endif
+// ---- The split-layout 32-slot front (AGATHA_SPLIT16, DESIGN.md §6.1 "Split layout") ----
+// Slot g of the band front lives in lane (g mod HS) / NREG, register g mod NREG, half
+// g / HS (HS = 32 * NREG): the low halves of the warp hold the first HS diagonals, the
+// high halves the next HS.  A lane's low and high cells of one register then sit HV =
+// HS / 2 positions apart along the anti-diagonal, so each register's substitution-score
+// pair (S_t, S_{t+HV}) is one table lookup of a selector pair precomputed per position:
+//   P(x) = c(R_x) | 0x80 | (c(R_{x+HV}) | 0x80) << 8     (c = 4-bit code, 8 outside R)
+//   W_R(x) = P(x) | P(x+1) << 16   (low: the PAR = 0 step, high: the PAR = 1 step)
+//   V_Q(y) = Pq(y) | Pq(y) << 16   (Pq likewise on the reversed Q)
+// combine(W_R, V_Q) holds both steps' selectors (nibbles 1 and 3 of each are 8: a zero
+// byte), so a register costs one LOP3 (both steps) and one PRMT per step, with no
+// funnel shifts or pair assembly.  The streams are written per pair into the work unit's
+// scratch (rw / qw) and copied, 15 words per lane and sequence per 8 iterations, into
+// per-lane shared-memory rows with cp.async (double-buffered, odd row stride: the
+// per-iteration LDS are bank-conflict free).  Both cross-lane exchanges become one
+// shuffle and one PRMT whose per-lane byte selector also inserts the band walls.
+constexpr int kRowW = 16;                 // words per lane row (8 iterations + 7, + 1 read ahead)
+constexpr int kRowS = 17;                 // row stride (odd: conflict-free LDS)
+__host__ __device__ inline long long s16_len(long long mn) {  // stream words for m + n
+  const long long nit = mn / 2 + 2, np = (nit + 7) / 8 + 2;
+  return 8 * np + 8 * 32 + 24;
+}
+__host__ __device__ inline long long s16_unit_words(long long mn) {  // words + bytes, per sequence
+  const long long L = s16_len(mn);
+  return L + (L + 264 + 3) / 4 + 8;
+}
+
+// The high half of a selector word in its low half, on the FMA pipe at full rate: an
+// fp16x2 add of -0.0 to the high half broadcast (HADD2 R, R.H1_H1, -RZ).  Exact: every
+// selector half is 0x8?8? (nibbles 1 and 3 are 8), a finite fp16 (exponent <= 3; small
+// ones are subnormal, which f16 arithmetic keeps without .ftz), and x + (-0) = x.  The
+// PRMT that consumes it reads only the low 16 bits.  (IMAD.HI, the alternative on the FMA
+// pipe, issues at a quarter rate.)
+#ifndef AGATHA_HSWAP
+#define AGATHA_HSWAP 1
+#endif
+__device__ __forceinline__ uint32_t hi_to_lo(uint32_t x, uint32_t k65536) {
+  if (!AGATHA_HSWAP) return shr16_fma(x, k65536);
+  uint32_t d;
+  asm("{\n\t.reg .b16 lo, hi;\n\t.reg .b32 t, z;\n\tmov.b32 {lo, hi}, %1;\n\tmov.b32 t, {hi, hi};\n\t"
+      "mov.b32 z, 0x80008000;\n\tadd.rn.f16x2 %0, t, z;\n\t}" : "=r"(d) : "r"(x));
+  return d;
+}
+__device__ __forceinline__ uint32_t lds_u32(unsigned addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ unsigned add_fma(unsigned a, unsigned b, unsigned one) {
+  unsigned d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(one), "r"(b));
+  return d;
+}
+
+template <int NREG, bool TRACE, int NCAP, bool ENDS = false>
+__device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap, uint32_t* rows,
+                              int unit, int* erec) {
+  constexpr int HS = 32 * NREG, HV = HS / 2, LC = NREG / 2;  // LC: cells per lane per half
+  constexpr int K = 2 * NREG;
+  const PairSrc ps = pair_src(A.own, A.ref_ascii, A.qry_ascii, A.roff, A.qoff, pid);
+  const uint64_t r0 = ps.r0, q0 = ps.q0;
+  const int m = (int)ps.m;
+  const int n = (int)ps.n;
+  if (A.bad[pid]) {
+    if (lane == 0) {
+      agatha_result_t z = {0, 0, 0, -1, 0};
+      A.out[pid] = z;
+    }
+    return;
+  }
+  const int bl = (A.bl < 0 || A.bl > n) ? n : A.bl;
+  const int br = (A.br < 0 || A.br > m) ? m : A.br;
+  const int alpha = A.alpha, beta = A.beta;
+  const int Dband = bl + br + 1;
+  const int off = (int)__reduce_max_sync(kFull, (unsigned)((-Dband) & (NREG - 1)));
+  const int dls = -bl - off;
+  const int gend = off + Dband;  // first slot above the band (a multiple of NREG)
+
+  // ---- a1: the selector streams of this pair ----
+  const int cb0 = dls & 1, u0 = (cb0 + dls) >> 1;
+  const int L = (int)s16_len((long long)m + n);
+  const int NP = (L - 8 * 32 - 24) / 8;  // periods the streams cover
+  const int ylo = n - u0 - 8 * NP - 7 + dls;
+  uint32_t* WR = A.rw + (uint64_t)(A.unit_base + unit) * A.rstride;
+  uint32_t* VQ = A.qw + (uint64_t)(A.unit_base + unit) * A.qstride;
+  {
+    if (A.ready) {
+      while (ld_acquire(A.ready + A.chunk_of[pid]) == 0) __nanosleep(500);
+    }
+    const bool nmap = A.nmap != 0;
+    int err = 0;
+    uint32_t* BR = WR + L;  // byte codes | 0x80: BR[ix] for x = u0 + ix, BQ[iy] for y = ylo + iy
+    uint32_t* BQ = VQ + L;
+    const int NBW = (L + 264) / 4;
+    const uint8_t* ref = ps.ref + r0;
+    const uint8_t* qry = ps.qry + q0;
+    for (int w = lane; w < NBW; w += 32) {
+      uint32_t br4 = 0, bq4 = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int x = u0 + 4 * w + t;  // R position (1-based)
+        uint32_t c = 8;
+        if (x >= 1 && x <= m) c = base_code(ref[x - 1], nmap, &err);
+        br4 |= (c | 0x80u) << (8 * t);
+        const int y = ylo + 4 * w + t;  // reversed-Q position: Q_{n - y}
+        c = 8;
+        if (y >= 0 && y < n) c = base_code(qry[n - 1 - y], nmap, &err);
+        bq4 |= (c | 0x80u) << (8 * t);
+      }
+      BR[w] = br4;
+      BQ[w] = bq4;
+    }
+    if (__any_sync(kFull, err) && lane == 0) atomicOr(A.err_flags, 1);
+    __syncwarp();
+    for (int a = lane; a < L / 4; a += 32) {
+      const uint32_t a0 = BR[a], a1 = BR[a + 1], c0 = BR[a + HV / 4], c1 = BR[a + HV / 4 + 1];
+      const uint32_t e0 = BQ[a], e1 = BQ[a + 1], f0 = BQ[a + HV / 4], f1 = BQ[a + HV / 4 + 1];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t u = __funnelshift_r(a0, a1, 8 * t), v = __funnelshift_r(c0, c1, 8 * t);
+        WR[4 * a + t] = prmt(u, v, 0x5140);
+        const uint32_t uq = __funnelshift_r(e0, e1, 8 * t), vq = __funnelshift_r(f0, f1, 8 * t);
+        VQ[4 * a + t] = prmt(uq, vq, 0x4040);
+      }
+    }
+    __syncwarp();
+  }
+  constexpr bool kRegWin = AGATHA_SPLITWIN != 0;
+  // per-lane rows: [buffer][R, Q][lane][kRowW] words
+  const unsigned rows_s = (unsigned)__cvta_generic_to_shared(rows);
+  auto row_addr = [&](int buf, int sq) { return rows_s + 4u * (unsigned)(((buf * 2 + sq) * 32 + lane) * kRowS); };
+  // period P's rows: R words of iterations 8P .. 8P+8, Q words of 8P .. 8P+8 (the Q row
+  // starts one word lower: the last iteration of a period reads the next one's first)
+  auto fill = [&](int P) {
+    const uint32_t* sR = WR + 8 * P + 8 * lane;
+    const uint32_t* sQ = VQ + 8 * (NP - P) + 8 * lane - 1;
+    const unsigned dR = row_addr(P & 1, 0), dQ = row_addr(P & 1, 1);
+#pragma unroll
+    for (int w = 0; w < kRowW; ++w) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dR + 4 * w), "l"(sR + w) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dQ + 4 * w), "l"(sQ + w) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (!kRegWin) {
+    fill(0);
+    fill(1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+  }
+
+  State16 s;
+  s.m = m; s.n = n; s.dlo = dls; s.D = Dband; s.alpha = alpha; s.beta = beta;
+  s.mn = (A.variant & AGATHA_VAR_CHECK_LAST) ? m + n + 1 : m + n;
+  s.zdrop = A.zdrop; s.B = -A.ref16; s.posValid = true;
+  s.G_H = INT_MIN / 2; s.G_c = 0; s.G_i = 0; s.G_j = 0; s.G_d = 0; s.zthr = INT_MIN;
+  if (A.variant & AGATHA_VAR_ORIGIN_MAX) {
+    s.G_H = 0;
+    s.zthr = A.zdrop >= 0 ? -A.zdrop : INT_MIN;
+  }
+  s.snapB = 0; s.snapPar = 0; s.snapTlo = 0; s.snapThi = 0; s.term = -1;
+  s.posC = 0;
+  s.zeff = A.zdrop >= 0 ? A.zdrop : (1 << 30);
+  const int dlo = -bl, D = Dband;
+  const uint32_t AmB2 = pack2(alpha - beta, alpha - beta);
+  // exchange byte selectors (prmt(v, W2, sel): bytes 0-3 of v, 4-7 of the wall W2)
+  uint32_t sel0 = lane == 0 ? (0x54u | (0x10u << 8)) : 0x3210u;
+  uint32_t s1lo = lane == 31 ? 0x32u : 0x10u, s1hi = lane == 31 ? 0x76u : 0x32u;
+  if (gend < 2 * HS) {  // the band top's left neighbour (slot gend) is the wall
+    const int gt = gend - 1;
+    if (lane == (gt % HS) / NREG) {
+      if (gt < HS) s1lo = 0x54u; else s1hi = 0x76u;
+    }
+  }
+  const uint32_t sel1 = s1lo | (s1hi << 8);
+  const uint32_t LMK = ((lane + 1) * NREG <= gend ? 0xFFFFu : 0u) | (HS + (lane + 1) * NREG <= gend ? 0xFFFF0000u : 0u);
+
+  auto fdiag = [&](int d) { return 2 * min(m, n + d) - d; };
+  const int dhi = br;
+  const int cs = 2 + max(bl, br);
+  const int ce = min(fdiag(dlo), fdiag(dhi));
+  const int dmid = min(max(m - n, dlo), dhi);
+  const int c_last = fdiag(dmid);
+  int cb = cb0;
+  auto bnd = [&](int d) { const int ad = d < 0 ? -d : d; return d == 0 ? 0 : -(alpha + (ad - 1) * beta); };
+
+  uint32_t H[NREG], E[NREG], F[NREG], CAP[CapMode<NCAP>::ncap];
+  const uint32_t W2 = pack2(kW16, kW16);
+#pragma unroll
+  for (int j = 0; j < NREG; ++j) {
+    int v2[2], c2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int g = h * HS + lane * NREG + j, d = dls + g;
+      const bool valid = g >= off && g < gend;
+      c2[h] = valid ? kTop16 + 127 : kCapNeg16;
+      const int ci = ((g & 1) == 0) ? cb - 2 : cb - 1;
+      v2[h] = valid ? (d == 0 ? 0 : bnd(d) + alpha * ci) - s.B : kCapNeg16;
+    }
+    H[j] = pack2(v2[0], v2[1]);
+    if (!CapMode<NCAP>::pin && j < NCAP) CAP[j < NCAP ? j : 0] = pack2(c2[0], c2[1]);
+    E[j] = W2;
+    F[j] = W2;
+  }
+  if (CapMode<NCAP>::pin) CAP[0] = pack2(lane == 0 ? kCapNeg16 : 0x7FFF, 0x7FFF);
+
+#ifndef AGATHA_SPLITPIN
+#define AGATHA_SPLITPIN 1
+#endif
+  // the table words pinned in vector registers (a volatile copy cannot be rematerialised
+  // from the uniform registers before every PRMT)
+  uint32_t T0, T1;
+  if (AGATHA_SPLITPIN) {
+    // T0 + lane * 0 (A.one - 1 is a run-time zero): a per-lane value lives in a vector
+    // register, which PRMT reads as its table operand with no copy from a uniform one
+    T0 = A.T16_0 + (uint32_t)lane * (A.one - 1u);
+    T1 = A.T16_1;
+  } else {
+    T0 = A.T16_0;
+    T1 = A.T16_1;
+  }
+  const uint32_t k65536 = A.k65536, one = A.one;
+  const int ref16 = -s.B;
+  int rH_prev = kEmpty16 - 1, B_prev = s.B, tlo_prev = 0, thi_prev = HV + LC - 1;
+  bool stop = false;
+  int iters = 0, it = 0, itc = 0;  // itc: index of the running iteration
+  // the row words of iteration ip of a period: R ip + k, Q 8 - ip + k; xs holds the next
+  // iteration's selector words, loaded one iteration ahead (the LDS latency hides behind
+  // the PAR = 1 step), aR / aQ the row addresses of the iteration after it
+  uint32_t xs[NREG / 2];
+  unsigned aR = row_addr(0, 0), aQ = row_addr(0, 1) + 4u * 8u;
+  // AGATHA_SPLITWIN: the words of iteration `it` sit in registers, wr[k] = W_R(u + 8 lane + k)
+  // and wq[k] = V_Q(n - u + dls + 8 lane + k); each iteration shifts them by one word
+  // (register moves on the FMA pipe) and loads the one new word of each from the
+  // stream (L1), one iteration ahead
+  uint32_t wr[kRegWin ? NREG / 2 : 1], wq[kRegWin ? NREG / 2 : 1], nr = 0, nq = 0;
+  const int iq0 = 8 * NP + 7 + 8 * lane;  // V_Q index of y(u0, k = 0)
+  // the new words of the next iteration (R ascending, Q descending); advanced with a
+  // 64-bit IMAD (mad.wide) on the FMA pipe
+  unsigned long long nextR = (unsigned long long)(WR + 8 * lane + 8), nextQ = (unsigned long long)(VQ + iq0 - 1);
+  const int oneV = (int)(one + (uint32_t)lane * (one - 1u));  // 1, per lane (not uniform)
+  auto adv = [&](unsigned long long p, int by) {
+    unsigned long long d;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(oneV), "r"(by), "l"(p));
+    return d;
+  };
+  if (kRegWin) {
+    nr = __ldca(reinterpret_cast<const uint32_t*>(nextR));
+    nq = __ldca(reinterpret_cast<const uint32_t*>(nextQ));
+    nextR = adv(nextR, 4);
+    nextQ = adv(nextQ, -4);
+  }
+  if (kRegWin) {
+#pragma unroll
+    for (int k = 0; k < NREG / 2; ++k) {
+      wr[k] = WR[8 * lane + k];
+      wq[k] = VQ[iq0 + k];
+    }
+  }
+  auto load_xs = [&]() {
+    if (kRegWin) {
+#pragma unroll
+      for (int k = 0; k < NREG / 2; ++k) xs[k] = combine(wr[k], wq[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NREG / 2; ++k) xs[k] = combine(lds_u32(aR + 4 * k), lds_u32(aQ + 4 * k));
+      aR = add_fma(aR, 4u, one);
+      aQ = add_fma(aQ, (unsigned)-4, one);
+    }
+  };
+  auto shift_win = [&](int itn) {  // -> the words of iteration itn; load those of itn + 1
+    if (kRegWin) {
+#pragma unroll
+      for (int k = 0; k < NREG / 2 - 1; ++k) wr[k] = wr[k + 1];
+      wr[NREG / 2 - 1] = nr;
+#pragma unroll
+      for (int k = NREG / 2 - 1; k > 0; --k) wq[k] = wq[k - 1];
+      wq[0] = nq;
+      nr = __ldca(reinterpret_cast<const uint32_t*>(nextR));
+      nq = __ldca(reinterpret_cast<const uint32_t*>(nextQ));
+      nextR = adv(nextR, 4);
+      nextQ = adv(nextQ, -4);
+    }
+  };
+  if (kRegWin) load_xs();
+  else load_xs();
+
+  // cells t in [tlo, thi] (t = k low, HV + k high) -> V2 bits k and 16 + k
+  auto valid_bits = [&](int tlo, int thi) {
+    auto run = [](int lo, int hi) -> uint32_t {
+      lo = max(lo, 0);
+      hi = min(hi, LC - 1);
+      if (hi < lo) return 0u;
+      return ((1u << (hi + 1)) - 1u) & ~((1u << lo) - 1u);
+    };
+    return run(tlo, thi) | (run(tlo - HV, thi - HV) << 16);
+  };
+  if (ENDS) {
+    if (lane == 0) ends_init(erec);
+    __syncwarp();
+  }
+  auto capture = [&](const uint32_t (&H)[NREG], int c, int P, int Bc) {
+    const int uc = (c - P + dls) >> 1;
+    const int ib = uc + P + lane * LC, jb = uc - dls - lane * LC;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      ends_capture(erec, ib + h * HV, jb - h * HV, LC, m, n,
+                   [&](int t) {
+                     uint32_t v = 0;
+#pragma unroll
+                     for (int k = 0; k < NREG / 2; ++k)
+                       if (k == t) v = P ? H[1 + 2 * k] : H[2 * k];
+                     const int st = h ? hi16(v) : lo16(v);
+                     return st - alpha * c + Bc;
+                   },
+                   [&](int t) {
+                     const int g = h * HS + lane * NREG + P + 2 * t;
+                     return g >= off && g < gend;
+                   });
+    }
+    __syncwarp();
+  };
+  auto iteration = [&](auto masked_tag) {
+    constexpr bool MASKED = decltype(masked_tag)::value;
+    uint32_t S2[NREG / 2], V2 = 0u;
+    const int u = (cb + dls) >> 1;
+    // ---- step PAR = 0, anti-diagonal cb ----
+    {
+#pragma unroll
+      for (int k = 0; k < NREG / 2; ++k) S2[k] = prmt(T0, T1, xs[k]);
+      int tlo = 0, thi = HV + LC - 1;
+      if (MASKED) {
+        const int ib = u + lane * LC, jb = u - dls - lane * LC;
+        tlo = max(1 - ib, jb - n);
+        thi = min(m - ib, jb - 1);
+        V2 = valid_bits(tlo, thi);
+      }
+      const uint32_t lmax = step16<NREG, NCAP, 0, MASKED, true>(H, H, H, E, F, CAP, S2, AmB2, lane, V2, k65536, one,
+                                                                sel1, LMK, sel0);
+      const int rH = warp_max16(lmax, k65536);
+      if (MASKED && ENDS) capture(H, cb - 1, 1, B_prev);
+      if (process16<NREG, 1, TRACE, !MASKED, true>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
+      rH_prev = rH;
+      if (!AGATHA_STEADYC || MASKED) {
+        B_prev = s.B;
+        tlo_prev = MASKED ? tlo : 0;
+        thi_prev = MASKED ? thi : HV + LC - 1;
+      }
+    }
+    // ---- step PAR = 1, anti-diagonal cb + 1 ----
+    {
+#pragma unroll
+      for (int k = 0; k < NREG / 2; ++k) S2[k] = prmt(T0, T1, hi_to_lo(xs[k], k65536));
+      if (kRegWin) {
+        shift_win(itc + 1);
+        load_xs();
+      } else {
+        load_xs();  // the next iteration's selectors (the rows of this period hold them)
+      }
+      int tlo = 0, thi = HV + LC - 1;
+      if (MASKED) {
+        const int ib = u + 1 + lane * LC, jb = u - dls - lane * LC;
+        tlo = max(1 - ib, jb - n);
+        thi = min(m - ib, jb - 1);
+        V2 = valid_bits(tlo, thi);
+      }
+      const uint32_t lmax = step16<NREG, NCAP, 1, MASKED, true>(H, H, H, E, F, CAP, S2, AmB2, lane, V2, k65536, one,
+                                                                sel1, LMK, sel0);
+      const int rH = warp_max16(lmax, k65536);
+      if (MASKED && ENDS) capture(H, cb, 0, B_prev);
+      if (process16<NREG, 0, TRACE, !MASKED, true>(s, A, cb, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid)) { stop = true; return; }
+      rH_prev = rH;
+      if (!AGATHA_STEADYC || MASKED) {
+        B_prev = s.B;
+        tlo_prev = MASKED ? tlo : 0;
+        thi_prev = MASKED ? thi : HV + LC - 1;
+      }
+    }
+    cb += 2;
+    ++itc;
+  };
+
+  auto housekeeping = [&]() {
+    if (!kRegWin && (it & 7) == 0) {  // period boundary: rows of the next period in, this one's ready
+      const int P = it >> 3;
+      fill(P + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      aR = row_addr(P & 1, 0) + 4u;  // xs already holds iteration 0 of period P
+      aQ = row_addr(P & 1, 1) + 4u * 7u;
+    }
+    if (iters >= kRebase16) {
+      iters = 0;
+      if (rH_prev > kEmpty16) {
+        const int delta = rH_prev + B_prev - s.B - ref16;
+        if (AGATHA_STEADYC) {
+          rH_prev -= delta - (B_prev - s.B);
+          B_prev = s.B + delta;
+        }
+        const uint32_t nd2 = pack2(-delta, -delta);
+#pragma unroll
+        for (int j = 0; j < NREG; ++j) {
+          H[j] = vaddmax2(H[j], nd2, W2);
+          if (j & 1) {
+            E[j] = vaddmax2(E[j], nd2, W2);
+            F[j] = vaddmax2(F[j], nd2, W2);
+          }
+        }
+        s.B += delta;
+      }
+      if (CapMode<NCAP>::pin) {
+#pragma unroll
+        for (int j = 0; j < CapMode<NCAP>::off - 1; ++j) {
+          H[j] = vmin2(H[j], CAP[0]);
+          if (j & 1) {
+            E[j] = vmin2(E[j], CAP[0]);
+            F[j] = vmin2(F[j], CAP[0]);
+          }
+        }
+      }
+    }
+  };
+  auto run_phase = [&](auto masked_tag, int total) {
+    while (!stop && total > 0) {
+      int k = 8 - (it & 7);
+      k = min(k, kRebase16 - iters);
+      k = min(k, total);
+      total -= k;
+      iters += k;
+      it += k;
+#pragma unroll 1
+      for (int t = 0; t < k; ++t) {
+        iteration(masked_tag);
+        if (stop) break;
+      }
+      housekeeping();
+    }
+  };
+  {
+    const int head_end = min(cs, c_last + 1);
+    run_phase(TrueT{}, cb < head_end ? (head_end - cb + 1) >> 1 : 0);
+    const int ce_s = ENDS ? ce - 1 : ce;
+    run_phase(FalseT{}, cb + 1 <= ce_s ? ((ce_s - cb + 1) >> 1) : 0);
+    run_phase(TrueT{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);
+  }
+  if (!kRegWin) asm volatile("cp.async.wait_all;" ::: "memory");  // no copy may land in the next pair's rows
+  if (!stop) {
+    if (ENDS) capture(H, cb - 1, 1, B_prev);
+    process16<NREG, 1, TRACE, false, true>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
+  }
+  if (ENDS && lane == 0) ends_store(A.ends + pid, erec);
+  resolve_G16<NREG, true>(s, snap, lane);
+
+  const int c_end = s.term >= 0 ? s.term : m + n;
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int g = (k / NREG) * HS + lane * NREG + (k % NREG);
+    if (g >= off && g < gend) {
+      const int d = dls + g;
+      const int clo = (d < 0 ? -d : d) + 2;
+      const int hi = min(fdiag(d), c_end);
+      if (hi >= clo) cnt += ((hi - clo) >> 1) + 1;
+    }
+  }
+  cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
+  if (lane == 0) {
+    agatha_result_t r;
+    r.score = s.G_H;
+    r.ref_end = s.G_i;
+    r.query_end = s.G_j;
+    r.zdrop_antidiag = s.term;
+    r.cells = cnt;
+    A.out[pid] = r;
+  }
+  (void)dlo; (void)D;
+}
+
 // Warps per block and blocks per SM of each front (A/B: AGATHA_WPB16 / AGATHA_MINB16)
 #ifndef AGATHA_WPB16
 #define AGATHA_WPB16 4
@@ -1770,6 +2302,8 @@ __device__ __forceinline__ void align16_body(const AlignArgs& A) {
   __shared__ uint32_t snap_all[Front16<NREG>::wpb][NREG / 2 * 32];
   __shared__ uint32_t pref_all[Front16<NREG>::wpb][64];
   __shared__ int erec_all[Front16<NREG>::wpb][8];  // NEXT #4 end-score records
+  constexpr bool kSplit = AGATHA_SPLIT16 && NREG == 16;
+  __shared__ __align__(16) uint32_t rows_all[kSplit ? Front16<NREG>::wpb : 1][kSplit ? 4 * 32 * kRowS : 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int unit = blockIdx.x * Front16<NREG>::wpb + warp, nunits = gridDim.x * Front16<NREG>::wpb;
   int k = 0;
@@ -1778,7 +2312,10 @@ __device__ __forceinline__ void align16_body(const AlignArgs& A) {
     if (lane == 0) q = claim_next(A, unit, nunits, k);
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
-    align_pair16<NREG, TRACE, NCAP, ENDS>(A, A.order[q], lane, snap_all[warp], pref_all[warp], unit, erec_all[warp]);
+    if constexpr (kSplit)
+      align_pair16s<NREG, TRACE, NCAP, ENDS>(A, A.order[q], lane, snap_all[warp], rows_all[warp], unit, erec_all[warp]);
+    else
+      align_pair16<NREG, TRACE, NCAP, ENDS>(A, A.order[q], lane, snap_all[warp], pref_all[warp], unit, erec_all[warp]);
   }
 }
 
@@ -2382,7 +2919,12 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   }
   // packing scratch per work unit: guard word + up to len/8 + 2 data words + guard word
   // (load_word_rw), rounded up to 32 B; the unit count is sized at the launches below
-  const uint64_t rstride = ((uint64_t)max_m / 8 + 4 + 7) & ~7ull, qstride = ((uint64_t)max_n / 8 + 4 + 7) & ~7ull;
+  uint64_t rstride = ((uint64_t)max_m / 8 + 4 + 7) & ~7ull, qstride = ((uint64_t)max_n / 8 + 4 + 7) & ~7ull;
+  if (AGATHA_SPLIT16) {  // the split 32-slot front's selector streams (align_pair16s)
+    const uint64_t w = ((uint64_t)s16_unit_words((long long)max_m + max_n) + 7) & ~7ull;
+    rstride = std::max(rstride, w);
+    qstride = std::max(qstride, w);
+  }
   if (err0 & 2) return AGATHA_EEMPTY;
   if (err0 & 4) return AGATHA_ERANGE;
 
