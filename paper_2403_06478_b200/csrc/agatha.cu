@@ -1789,6 +1789,9 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 #ifndef AGATHA_SPLIT16
 #define AGATHA_SPLIT16 1  // 0: the 32-slot front keeps the paired (j, j + NREG) layout
 #endif
+#ifndef AGATHA_SPLITU2
+#define AGATHA_SPLITU2 0  // split front: steady loop trips of two iterations
+#endif
 #ifndef AGATHA_SPLITWIN
 #define AGATHA_SPLITWIN 1  // split front: 1 register windows fed from the streams, 0 smem rows
 #endif
@@ -2214,16 +2217,29 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
   };
   auto run_phase = [&](auto masked_tag, int total) {
     while (!stop && total > 0) {
-      int k = 8 - (it & 7);
-      k = min(k, kRebase16 - iters);
+      // (register windows need no period boundary: runs end at re-centrings only)
+      int k = kRegWin ? kRebase16 - iters : min(8 - (it & 7), kRebase16 - iters);
       k = min(k, total);
       total -= k;
       iters += k;
       it += k;
+      if (AGATHA_SPLITU2 && !decltype(masked_tag)::value) {
+        // steady runs two iterations per trip: the window shift by two words renames
+        // registers in the copies instead of moving them
 #pragma unroll 1
-      for (int t = 0; t < k; ++t) {
-        iteration(masked_tag);
-        if (stop) break;
+        for (int t = 0; t + 1 < k; t += 2) {
+          iteration(masked_tag);
+          if (stop) break;
+          iteration(masked_tag);
+          if (stop) break;
+        }
+        if (!stop && (k & 1)) iteration(masked_tag);
+      } else {
+#pragma unroll 1
+        for (int t = 0; t < k; ++t) {
+          iteration(masked_tag);
+          if (stop) break;
+        }
       }
       housekeeping();
     }
