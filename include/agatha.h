@@ -161,6 +161,9 @@ typedef struct {
                              group (they arrive before the queue reaches them)           */
   int32_t pin_off;     /* 32-slot front: the common low padding off = (-D) mod 16 of its
                           pairs when the pinned front ran (one capped slot), else -1     */
+  int32_t rebase_iters; /* 16-bit kernels: iterations between re-centrings of the 32-slot
+                          front (128, 64 or 32, the longest the 16-bit guard admits), 0
+                          when the 16-bit kernels do not apply                           */
 } agatha_stats_t;
 
 /* Create a context on CUDA device `cuda_device`.  Fails with AGATHA_ECUDA when the

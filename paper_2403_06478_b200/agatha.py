@@ -58,7 +58,8 @@ class Stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int32), ("library_launches", ctypes.c_int32),
                 ("packed16", ctypes.c_int32), ("warps_per_pair", ctypes.c_int32),
                 ("tier_pairs", ctypes.c_int32 * 3), ("input_chunks", ctypes.c_int32),
-                ("lpt_from_chunk", ctypes.c_int32), ("pin_off", ctypes.c_int32)]
+                ("lpt_from_chunk", ctypes.c_int32), ("pin_off", ctypes.c_int32),
+                ("rebase_iters", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: (list(v) if k == "tier_pairs" else v)

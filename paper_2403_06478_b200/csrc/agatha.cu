@@ -128,6 +128,7 @@ struct AlignArgs {
   uint32_t T16_0, T16_1;     // 16-bit kernel table: byte x = S + 2*alpha
   uint32_t k65536;           // the constant 65536, passed at run time (see shr16_fma)
   uint32_t one;              // the constant 1, passed at run time (see add16x2_fma)
+  int rebase16;              // split 32-slot front: iterations between re-centrings
   int ref16;                 // 16-bit kernel: stored value of the anti-diagonal max after
                              // a re-centring (negative)
 };
@@ -2020,6 +2021,7 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
   int rH_prev = kEmpty16 - 1, B_prev = s.B, tlo_prev = 0, thi_prev = HV + LC - 1;
   bool stop = false;
   int iters = 0, it = 0, itc = 0;  // itc: index of the running iteration
+  const int rebase = kRegWin ? A.rebase16 : kRebase16;  // iterations between re-centrings
   // the row words of iteration ip of a period: R ip + k, Q 8 - ip + k; xs holds the next
   // iteration's selector words, loaded one iteration ahead (the LDS latency hides behind
   // the PAR = 1 step), aR / aQ the row addresses of the iteration after it
@@ -2184,7 +2186,7 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
       aR = row_addr(P & 1, 0) + 4u;  // xs already holds iteration 0 of period P
       aQ = row_addr(P & 1, 1) + 4u * 7u;
     }
-    if (iters >= kRebase16) {
+    if (iters >= rebase) {
       iters = 0;
       if (rH_prev > kEmpty16) {
         const int delta = rH_prev + B_prev - s.B - ref16;
@@ -2218,7 +2220,7 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
   auto run_phase = [&](auto masked_tag, int total) {
     while (!stop && total > 0) {
       // (register windows need no period boundary: runs end at re-centrings only)
-      int k = kRegWin ? kRebase16 - iters : min(8 - (it & 7), kRebase16 - iters);
+      int k = kRegWin ? rebase - iters : min(8 - (it & 7), rebase - iters);
       k = min(k, total);
       total -= k;
       iters += k;
@@ -2581,44 +2583,58 @@ void score_table(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
 // half-word range with margin, and S + 2*alpha must fit the int8 score table.
 // the anti-diagonal max sits at ref16 after a re-centring; every stored H
 // stays in (kEmpty16, kTop16] and every wall/cap value above -32768.
-static long long drift16(const agatha_params_t* p) {
+static long long drift16(const agatha_params_t* p, int iv = kRebase16) {
   const long long mx = std::max<long long>(p->match, std::max<long long>(p->mismatch, p->ambig));
-  return (2 * kRebase16 + 6) * (2 * (long long)p->gap_open + mx);  // 70 at 32 iterations
+  return (2 * (long long)iv + 6) * (2 * (long long)p->gap_open + mx);  // 70 at 32 iterations
 }
 // Cells outside the table may rise above the anti-diagonal max of the valid cells by at
 // most (alpha - beta) per anti-diagonal for as long as they stay outside (at most
 // maxD + 2 anti-diagonals); the ref16 margin covers that, the drift between
 // re-centrings and the largest table entry, so every stored H stays <= kTop16.
-static int ref16_of(const agatha_params_t* p, int maxD) {
+static int ref16_of(const agatha_params_t* p, int maxD, int iv = kRebase16) {
   const long long a = p->match, al = p->gap_open, be = p->gap_extend;
   const long long mx = std::max<long long>(a, std::max<long long>(p->mismatch, p->ambig));
-  return (int)(kTop16 - 127 - (drift16(p) + 3 * al + 2 * a + mx + (al - be) * ((long long)maxD + 2)));
+  return (int)(kTop16 - 127 - (drift16(p, iv) + 3 * al + 2 * a + mx + (al - be) * ((long long)maxD + 2)));
 }
 // Pinned fronts (CapMode): between two re-centrings (kRebase16 iterations) the dead
 // padding slots, pinned at kCapNeg16 at the last one, rise by at most kRebase16 times
 // max(S + 2 alpha, 2 (alpha - beta)) in stored units (a diagonal move every two
 // anti-diagonals, or a gap extension every one); they must stay below kEmpty16.
-static bool pin16_ok(const agatha_params_t* p) {
+static bool pin16_ok(const agatha_params_t* p, int iv) {
   const long long al = p->gap_open, be = p->gap_extend;
   const long long mx = std::max<long long>(p->match, std::max<long long>(-p->mismatch, -p->ambig)) + 2 * al;
   const long long g = std::max<long long>(mx, 2 * (al - be));
-  return (kRebase16 + 1) * g + 2 * g < kEmpty16 - kCapNeg16;
+  return ((long long)iv + 1) * g + 2 * g < kEmpty16 - kCapNeg16;
 }
 // the common off = (-D) mod 16 of a launch's pairs, or -1 when they differ
 static int pin_off(int mask) { return (mask != 0 && (mask & (mask - 1)) == 0) ? __builtin_ctz(mask) : -1; }
-bool use16(const agatha_params_t* p, int maxD) {
+bool use16(const agatha_params_t* p, int maxD, int iv = kRebase16) {
   const long long a = p->match, al = p->gap_open, be = p->gap_extend;
   const long long mx = std::max<long long>(a, std::max<long long>(p->mismatch, p->ambig));
   const long long spread = al + (long long)maxD * (be + a + mx) + 4 * mx;
-  const long long drift = drift16(p);
+  const long long drift = drift16(p, iv);
   // int8 table entries S + 2*alpha must lie in [0, 127] (add16x2_fma); alpha >= beta
   // (the boundary chains of the masked steps)
   if (a + 2 * al > 127 || 2 * al - p->mismatch < 0 || 2 * al - p->ambig < 0 || al < be) return false;
   // a one-diagonal band (bl = br = 0) leaves every other anti-diagonal empty, so the
   // re-centring (on the last anti-diagonal's max) would never run
   if (p->band_left == 0 && p->band_right == 0) return false;
-  const long long ref = ref16_of(p, maxD);
+  const long long ref = ref16_of(p, maxD, iv);
   return ref - (spread + drift) > kEmpty16 && kW16 - drift > -32768 && maxD <= kMaxSlots;
+}
+
+// The 16-bit kernels' re-centring interval (iterations): the split 32-slot front takes the
+// longest of AGATHA_REBASE_MAX, ..., 64, 32 for which the 16-bit guard holds (a longer
+// interval means fewer loop runs but a larger drift term); the other
+// fronts re-centre every kRebase16 = 32, which the same ref16 covers (drift16 grows with
+// the interval).  0: the 16-bit kernels do not apply.
+#ifndef AGATHA_REBASE_MAX
+#define AGATHA_REBASE_MAX 128
+#endif
+static int rebase16_for(const agatha_params_t* p, int maxD) {
+  for (int iv = AGATHA_REBASE_MAX; iv >= kRebase16; iv /= 2)
+    if (use16(p, maxD, iv)) return iv;
+  return 0;
 }
 
 void score_table16(const agatha_params_t* p, uint32_t* T0, uint32_t* T1) {
@@ -2925,9 +2941,11 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   const int tier_n[3] = {ctx->h_scalars[4], ctx->h_scalars[5], ctx->h_scalars[6]};
   const int maxoff16_t0 = ctx->h_scalars[7];
   // the pinned 32-slot front (CapMode) when every pair of the launch has one off
-  const int pin_all = pin16_ok(p) ? pin_off(ctx->h_scalars[10]) : -1;
+  const int iv16 = rebase16_for(p, maxD);
+  const int pin_all = pin16_ok(p, iv16) ? pin_off(ctx->h_scalars[10]) : -1;
   ctx->stats.pin_off = -1;
-  const int pin_t0 = pin16_ok(p) ? pin_off(ctx->h_scalars[11]) : -1;
+  ctx->stats.rebase_iters = iv16;
+  const int pin_t0 = pin16_ok(p, iv16) ? pin_off(ctx->h_scalars[11]) : -1;
   const int max_m = ctx->h_scalars[16], max_n = ctx->h_scalars[17];
   if (dev_in) {
     tot_r = h_tot[0];
@@ -2945,7 +2963,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   if (err0 & 4) return AGATHA_ERANGE;
 
   const int K = maxD <= 512 ? 16 : 32;
-  const bool k16 = use16(p, maxD) && !(b->flags & AGATHA_FORCE_32BIT);
+  const bool k16 = iv16 > 0 && !(b->flags & AGATHA_FORCE_32BIT);
   if ((err0 & 8) && !k16) return AGATHA_ERANGE;  // a pair the 32-bit kernels cannot hold
   if (b->queue) {
     // Participants of a shared queue claim positions of ONE order with one counter per
@@ -3021,7 +3039,8 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   A.variant = p->variant;
   A.k65536 = 65536u;
   A.one = 1u;
-  A.ref16 = ref16_of(p, maxD);
+  A.ref16 = ref16_of(p, maxD, iv16 > 0 ? iv16 : kRebase16);
+  A.rebase16 = iv16 > 0 ? iv16 : kRebase16;
   score_table(p, &A.T0, &A.T1);
   score_table16(p, &A.T16_0, &A.T16_1);
   A.trace_pair = trace_pair; A.trace_score = trace_score; A.trace_i = trace_i; A.trace_cap = trace_cap;

@@ -99,6 +99,36 @@ def test_scoring_near_the_guard(gpu_lib, ctx):
                                    band_left=500, band_right=500, zdrop=-1), expect16=False)
 
 
+@pytest.mark.parametrize("sc,D,iv", [((2, 4, 4, 2), 1001, 128), ((2, 4, 6, 1), 1001, 64),
+                                     ((3, 5, 6, 2), 1001, 32), ((4, 6, 6, 3), 801, 32),
+                                     ((1, 3, 8, 2), 601, 64)])
+def test_recentring_intervals(gpu_lib, ctx, sc, D, iv):
+    """The 32-slot front re-centres every 128, 64 or 32 iterations, the longest interval the
+    16-bit guard admits for the scoring and band (the drift term grows with
+    the interval); every interval is bit-exact with the oracle, with and without Z-drop."""
+    a, b, go, ge = sc
+    rng = np.random.default_rng(31 + D + iv)
+    lst = []
+    for k in range(16):
+        r = rand_seq(rng, int(rng.integers(2000, 5000)))
+        q = "".join(c if rng.random() > 0.12 else "ACGT"[int(rng.integers(0, 4))] for c in r)
+        if k % 4 == 1:
+            x = int(rng.integers(200, 1500))
+            q = q[:x] + q[x + int(rng.integers(5, 120)):]
+        if k % 4 == 2:  # chimeric tail
+            cut = int(rng.integers(len(q) // 3, len(q)))
+            q = q[:cut] + rand_seq(rng, len(q) - cut)
+        lst.append((r, q))
+    pairs = synth.from_list(lst)
+    bl = (D - 1) // 2
+    for z in (-1, 150):
+        params = dict(match=a, mismatch=b, ambig=b, gap_open=go, gap_extend=ge,
+                      band_left=bl, band_right=D - 1 - bl, zdrop=z)
+        both(gpu_lib, ctx, pairs, params, expect16=True)
+        got = gpu_lib.align_pairs(ctx, pairs, params)
+        assert ctx.stats()["rebase_iters"] == iv, ctx.stats()
+
+
 def test_negative_stretches(gpu_lib, ctx):
     rng = np.random.default_rng(24)
     lst = [("N" * 3000, "N" * 2800), ("A" * 2000, "C" * 2000),
