@@ -56,10 +56,17 @@ LANES_PER_CLK_PER_SM = 64
 # SURVEY.md §8(d) roofline: I_cell = 9 int32 lane-instructions per cell (Eq. 1-3 + Eq. 5 on
 # sm_100a) against the measured integer lane-instruction rate P_int; the .S16x2 datapath
 # the 16-bit kernel runs carries two cells per lane-instruction, so its peak counts two
-# int16 lane-ops per lane-instruction (stated in the line).  P_int measured on the B200:
-# VIADDMNMX/VIMNMX3 .S16x2 62.4 lanes/clk/SM (profiles/r01_dpx16.jsonl).
+# int16 lane-ops per lane-instruction (stated in the line).  P_int measured on the B200
+# (profiles/r01_int_pipes.jsonl): the highest sustained integer lane-instruction rate of
+# the SM, 89.0 lanes/clk/SM (IADD3 at 32 warps/SM, which issues to both the ALU and the
+# FMA pipe; an IMNMX + IMAD 1:1 mix reaches 88.1), since the kernel uses both pipes (the
+# Eq. 1 add and the selector shifts run on the FMA pipe).  The ALU pipe alone sustains
+# 62.4 (VIADDMNMX/VIMNMX3 .S16x2, profiles/r01_dpx16.jsonl): the fraction against that
+# is printed too (frac_alu_pipe_only; it exceeds 1 once the kernel needs fewer than
+# I_cell / 2 ALU-pipe instructions per cell).
 I_CELL = 9
-P_INT_LANES_PER_CLK_PER_SM = 62.4
+P_INT_LANES_PER_CLK_PER_SM = 89.0
+P_ALU_LANES_PER_CLK_PER_SM = 62.4
 PAPER_SPEEDUP = {"value": 18.8, "what": "AGAThA vs minimap2 extension (geometric mean over 9 datasets)",
                  "gpu": "NVIDIA RTX A6000", "cpu": "AMD EPYC 7313P 16C/32T, minimap2 SSE4.1",
                  "cite": "PAPER.md l.600-602 (setup), l.673 (18.8x), l.830 (16C32T SSE4)",
@@ -587,6 +594,7 @@ def main():
     # lane-ops per lane-instruction), x 1 for the 32-bit kernels
     lanes_per_instr = 2 if packed16 else 1
     peak_tops = SM_COUNT * P_INT_LANES_PER_CLK_PER_SM * lanes_per_instr * f_ghz * 1e9 / 1e12
+    peak_alu_tops = SM_COUNT * P_ALU_LANES_PER_CLK_PER_SM * lanes_per_instr * f_ghz * 1e9 / 1e12
     achieved_tops = I_CELL * kernel_gcups * 1e9 / 1e12
     # the builder's tighter roof: the minimal ALU-pipe instruction count of this kernel's
     # formulation, against 64 ALU lanes/clk/SM
@@ -596,16 +604,23 @@ def main():
                 "unit": "T int lane-ops/s", "frac": achieved_tops / peak_tops,
                 "kernel": kname, "kernel_ms": align_avg_ms, "kernel_gcups": kernel_gcups,
                 "basis": (f"SURVEY.md §8(d): I_cell = {I_CELL} int lane-ops per cell; peak = 148 SM x "
-                          f"{P_INT_LANES_PER_CLK_PER_SM} lane-instr/clk/SM (measured, profiles/r01_dpx16.jsonl) x "
+                          f"{P_INT_LANES_PER_CLK_PER_SM} integer lane-instr/clk/SM (the SM's highest measured "
+                          f"integer rate, ALU + FMA pipes, profiles/r01_int_pipes.jsonl) x "
                           f"{lanes_per_instr} ({'.S16x2: two int16 lane-ops per lane-instruction' if packed16 else 'int32'})"
                           f" x {f_ghz:.3f} GHz (clocks.max.sm)"),
                 "gcups_roof": peak_tops * 1e12 / I_CELL / 1e9,
+                "frac_alu_pipe_only": achieved_tops / peak_alu_tops,
+                "alu_pipe_only_basis": f"the same against the ALU pipe alone, {P_ALU_LANES_PER_CLK_PER_SM} "
+                                       "lane-instr/clk/SM (profiles/r01_dpx16.jsonl)",
                 "alu_minimum": {"ops_per_cell": ops, "gcups_roof": alu_peak * 1e12 / ops / 1e9,
                                 "frac": kernel_gcups * 1e9 * ops / (alu_peak * 1e12),
                                 "basis": "minimal ALU-pipe lane-instructions per cell of this kernel's "
                                          "formulation (DESIGN.md §6.3) vs 148 SM x 64 ALU lanes/clk"}}
     # traffic and pipe utilisation from the newest committed ncu captures of this kernel
-    dram = newest_profile("*ncu*dram*.csv")
+    # (kernel-specific file names: the 16-bit kernels' captures are *ncu_align16_*, the
+    # wide tier's *ncu_align_wide*, the 32-bit one-warp kernel's *ncu_align_kernel*)
+    kfile = "align16" if packed16 else ("align_wide" if stats.get("warps_per_pair", 1) > 1 else "align_kernel")
+    dram = newest_profile(f"*ncu_{kfile}*dram*.csv")
     if dram:
         m = ncu_kernel_metrics(dram, ksub)
         if "dram__bytes_read.sum" in m:
@@ -614,7 +629,7 @@ def main():
             roofline["traffic_unit"] = "bytes/launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
     if "traffic" not in roofline:
         roofline["traffic"] = None
-    full_sum = newest_profile("*ncu*full_summary.csv")
+    full_sum = newest_profile(f"*ncu_{kfile}*full_summary.csv")
     if full_sum:
         m = ncu_kernel_metrics(full_sum, ksub)
         key = "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"
