@@ -1790,11 +1790,11 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 #ifndef AGATHA_SPLIT16
 #define AGATHA_SPLIT16 1  // 0: the 32-slot front keeps the paired (j, j + NREG) layout
 #endif
+#ifndef AGATHA_STREAM_PF
+#define AGATHA_STREAM_PF 256  // split front: L2 prefetch distance of the stream loads (words), 0 = none
+#endif
 #ifndef AGATHA_SPLITU2
 #define AGATHA_SPLITU2 0  // split front: steady loop trips of two iterations
-#endif
-#ifndef AGATHA_SPLITWIN
-#define AGATHA_SPLITWIN 1  // split front: 1 register windows fed from the streams, 0 smem rows
 #endif
 // ---- The split-layout 32-slot front (AGATHA_SPLIT16, DESIGN.md §6.1 "Split layout") ----
 // Slot g of the band front lives in lane (g mod HS) / NREG, register g mod NREG, half
@@ -1808,19 +1808,21 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 // combine(W_R, V_Q) holds both steps' selectors (nibbles 1 and 3 of each are 8: a zero
 // byte), so a register costs one LOP3 (both steps) and one PRMT per step, with no
 // funnel shifts or pair assembly.  The streams are written per pair into the work unit's
-// scratch (rw / qw) and copied, 15 words per lane and sequence per 8 iterations, into
-// per-lane shared-memory rows with cp.async (double-buffered, odd row stride: the
-// per-iteration LDS are bank-conflict free).  Both cross-lane exchanges become one
-// shuffle and one PRMT whose per-lane byte selector also inserts the band walls.
-constexpr int kRowW = 16;                 // words per lane row (8 iterations + 7, + 1 read ahead)
-constexpr int kRowS = 17;                 // row stride (odd: conflict-free LDS)
+// scratch (rw / qw); each lane keeps its eight R and eight Q words of an iteration in
+// registers and loads one new word of each per iteration.  Both cross-lane exchanges
+// become one shuffle and one PRMT whose per-lane byte selector also inserts the walls.
+constexpr int kStreamPad = 256;    // >= AGATHA_STREAM_PF
+static_assert(kStreamPad >= AGATHA_STREAM_PF, "stream prefetches must stay inside a unit");
 __host__ __device__ inline long long s16_len(long long mn) {  // stream words for m + n
   const long long nit = mn / 2 + 2, np = (nit + 7) / 8 + 2;
   return 8 * np + 8 * 32 + 24;
 }
 __host__ __device__ inline long long s16_unit_words(long long mn) {  // words + bytes, per sequence
   const long long L = s16_len(mn);
-  return L + (L + 264 + 3) / 4 + 8;
+  // + kStreamPad: the Q stream starts kStreamPad words into its unit and both streams end
+  // at least that far before the unit's end, so the L2 prefetches (AGATHA_STREAM_PF words
+  // ahead of a read) stay inside the unit's own scratch
+  return L + (L + 264 + 3) / 4 + 8 + 2 * kStreamPad;
 }
 
 // The high half of a selector word in its low half, on the FMA pipe at full rate: an
@@ -1839,20 +1841,8 @@ __device__ __forceinline__ uint32_t hi_to_lo(uint32_t x, uint32_t k65536) {
       "mov.b32 z, 0x80008000;\n\tadd.rn.f16x2 %0, t, z;\n\t}" : "=r"(d) : "r"(x));
   return d;
 }
-__device__ __forceinline__ uint32_t lds_u32(unsigned addr) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ unsigned add_fma(unsigned a, unsigned b, unsigned one) {
-  unsigned d;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(one), "r"(b));
-  return d;
-}
-
 template <int NREG, bool TRACE, int NCAP, bool ENDS = false>
-__device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap, uint32_t* rows,
-                              int unit, int* erec) {
+__device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32_t* snap, int unit, int* erec) {
   constexpr int HS = 32 * NREG, HV = HS / 2, LC = NREG / 2;  // LC: cells per lane per half
   constexpr int K = 2 * NREG;
   const PairSrc ps = pair_src(A.own, A.ref_ascii, A.qry_ascii, A.roff, A.qoff, pid);
@@ -1880,7 +1870,7 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
   const int NP = (L - 8 * 32 - 24) / 8;  // periods the streams cover
   const int ylo = n - u0 - 8 * NP - 7 + dls;
   uint32_t* WR = A.rw + (uint64_t)(A.unit_base + unit) * A.rstride;
-  uint32_t* VQ = A.qw + (uint64_t)(A.unit_base + unit) * A.qstride;
+  uint32_t* VQ = A.qw + (uint64_t)(A.unit_base + unit) * A.qstride + kStreamPad;
   {
     if (A.ready) {
       while (ld_acquire(A.ready + A.chunk_of[pid]) == 0) __nanosleep(500);
@@ -1923,29 +1913,6 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
     }
     __syncwarp();
   }
-  constexpr bool kRegWin = AGATHA_SPLITWIN != 0;
-  // per-lane rows: [buffer][R, Q][lane][kRowW] words
-  const unsigned rows_s = (unsigned)__cvta_generic_to_shared(rows);
-  auto row_addr = [&](int buf, int sq) { return rows_s + 4u * (unsigned)(((buf * 2 + sq) * 32 + lane) * kRowS); };
-  // period P's rows: R words of iterations 8P .. 8P+8, Q words of 8P .. 8P+8 (the Q row
-  // starts one word lower: the last iteration of a period reads the next one's first)
-  auto fill = [&](int P) {
-    const uint32_t* sR = WR + 8 * P + 8 * lane;
-    const uint32_t* sQ = VQ + 8 * (NP - P) + 8 * lane - 1;
-    const unsigned dR = row_addr(P & 1, 0), dQ = row_addr(P & 1, 1);
-#pragma unroll
-    for (int w = 0; w < kRowW; ++w) {
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dR + 4 * w), "l"(sR + w) : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dQ + 4 * w), "l"(sQ + w) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  if (!kRegWin) {
-    fill(0);
-    fill(1);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-  }
-
   State16 s;
   s.m = m; s.n = n; s.dlo = dls; s.D = Dband; s.alpha = alpha; s.beta = beta;
   s.mn = (A.variant & AGATHA_VAR_CHECK_LAST) ? m + n + 1 : m + n;
@@ -2021,17 +1988,13 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
   int rH_prev = kEmpty16 - 1, B_prev = s.B, tlo_prev = 0, thi_prev = HV + LC - 1;
   bool stop = false;
   int iters = 0, it = 0, itc = 0;  // itc: index of the running iteration
-  const int rebase = kRegWin ? A.rebase16 : kRebase16;  // iterations between re-centrings
-  // the row words of iteration ip of a period: R ip + k, Q 8 - ip + k; xs holds the next
-  // iteration's selector words, loaded one iteration ahead (the LDS latency hides behind
-  // the PAR = 1 step), aR / aQ the row addresses of the iteration after it
+  const int rebase = A.rebase16;  // iterations between re-centrings (<= 128)
   uint32_t xs[NREG / 2];
-  unsigned aR = row_addr(0, 0), aQ = row_addr(0, 1) + 4u * 8u;
-  // AGATHA_SPLITWIN: the words of iteration `it` sit in registers, wr[k] = W_R(u + 8 lane + k)
+  // the words of iteration `it` sit in registers, wr[k] = W_R(u + 8 lane + k)
   // and wq[k] = V_Q(n - u + dls + 8 lane + k); each iteration shifts them by one word
   // (register moves on the FMA pipe) and loads the one new word of each from the
   // stream (L1), one iteration ahead
-  uint32_t wr[kRegWin ? NREG / 2 : 1], wq[kRegWin ? NREG / 2 : 1], nr = 0, nq = 0;
+  uint32_t wr[NREG / 2], wq[NREG / 2], nr = 0, nq = 0;
   const int iq0 = 8 * NP + 7 + 8 * lane;  // V_Q index of y(u0, k = 0)
   // the new words of the next iteration (R ascending, Q descending); advanced with a
   // 64-bit IMAD (mad.wide) on the FMA pipe
@@ -2042,32 +2005,22 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
     asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(oneV), "r"(by), "l"(p));
     return d;
   };
-  if (kRegWin) {
-    nr = __ldca(reinterpret_cast<const uint32_t*>(nextR));
-    nq = __ldca(reinterpret_cast<const uint32_t*>(nextQ));
-    nextR = adv(nextR, 4);
-    nextQ = adv(nextQ, -4);
-  }
-  if (kRegWin) {
+  nr = __ldca(reinterpret_cast<const uint32_t*>(nextR));
+  nq = __ldca(reinterpret_cast<const uint32_t*>(nextQ));
+  nextR = adv(nextR, 4);
+  nextQ = adv(nextQ, -4);
 #pragma unroll
-    for (int k = 0; k < NREG / 2; ++k) {
-      wr[k] = WR[8 * lane + k];
-      wq[k] = VQ[iq0 + k];
-    }
+  for (int k = 0; k < NREG / 2; ++k) {
+    wr[k] = WR[8 * lane + k];
+    wq[k] = VQ[iq0 + k];
   }
   auto load_xs = [&]() {
-    if (kRegWin) {
 #pragma unroll
-      for (int k = 0; k < NREG / 2; ++k) xs[k] = combine(wr[k], wq[k]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < NREG / 2; ++k) xs[k] = combine(lds_u32(aR + 4 * k), lds_u32(aQ + 4 * k));
-      aR = add_fma(aR, 4u, one);
-      aQ = add_fma(aQ, (unsigned)-4, one);
-    }
+    for (int k = 0; k < NREG / 2; ++k) xs[k] = combine(wr[k], wq[k]);
   };
   auto shift_win = [&](int itn) {  // -> the words of iteration itn; load those of itn + 1
-    if (kRegWin) {
+    (void)itn;  // (kept: the counter shapes ptxas's loop code)
+    {
 #pragma unroll
       for (int k = 0; k < NREG / 2 - 1; ++k) wr[k] = wr[k + 1];
       wr[NREG / 2 - 1] = nr;
@@ -2076,12 +2029,15 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
       wq[0] = nq;
       nr = __ldca(reinterpret_cast<const uint32_t*>(nextR));
       nq = __ldca(reinterpret_cast<const uint32_t*>(nextQ));
+      if (AGATHA_STREAM_PF) {  // the streams' lines a few hundred iterations ahead into L2
+        asm volatile("prefetch.global.L2 [%0];" :: "l"(nextR + 4 * AGATHA_STREAM_PF));
+        asm volatile("prefetch.global.L2 [%0];" :: "l"(nextQ - 4 * AGATHA_STREAM_PF));
+      }
       nextR = adv(nextR, 4);
       nextQ = adv(nextQ, -4);
     }
   };
-  if (kRegWin) load_xs();
-  else load_xs();
+  load_xs();
 
   // cells t in [tlo, thi] (t = k low, HV + k high) -> V2 bits k and 16 + k
   auto valid_bits = [&](int tlo, int thi) {
@@ -2149,12 +2105,8 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
     {
 #pragma unroll
       for (int k = 0; k < NREG / 2; ++k) S2[k] = prmt(T0, T1, hi_to_lo(xs[k], k65536));
-      if (kRegWin) {
-        shift_win(itc + 1);
-        load_xs();
-      } else {
-        load_xs();  // the next iteration's selectors (the rows of this period hold them)
-      }
+      shift_win(itc + 1);
+      load_xs();
       int tlo = 0, thi = HV + LC - 1;
       if (MASKED) {
         const int ib = u + 1 + lane * LC, jb = u - dls - lane * LC;
@@ -2179,13 +2131,6 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
   };
 
   auto housekeeping = [&]() {
-    if (!kRegWin && (it & 7) == 0) {  // period boundary: rows of the next period in, this one's ready
-      const int P = it >> 3;
-      fill(P + 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-      aR = row_addr(P & 1, 0) + 4u;  // xs already holds iteration 0 of period P
-      aQ = row_addr(P & 1, 1) + 4u * 7u;
-    }
     if (iters >= rebase) {
       iters = 0;
       if (rH_prev > kEmpty16) {
@@ -2220,7 +2165,7 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
   auto run_phase = [&](auto masked_tag, int total) {
     while (!stop && total > 0) {
       // (register windows need no period boundary: runs end at re-centrings only)
-      int k = kRegWin ? rebase - iters : min(8 - (it & 7), rebase - iters);
+      int k = rebase - iters;
       k = min(k, total);
       total -= k;
       iters += k;
@@ -2253,7 +2198,6 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
     run_phase(FalseT{}, cb + 1 <= ce_s ? ((ce_s - cb + 1) >> 1) : 0);
     run_phase(TrueT{}, cb <= c_last ? ((c_last - cb) >> 1) + 1 : 0);
   }
-  if (!kRegWin) asm volatile("cp.async.wait_all;" ::: "memory");  // no copy may land in the next pair's rows
   if (!stop) {
     if (ENDS) capture(H, cb - 1, 1, B_prev);
     process16<NREG, 1, TRACE, false, true>(s, A, cb - 1, rH_prev, B_prev, tlo_prev, thi_prev, H, lane, snap, pid);
@@ -2321,7 +2265,6 @@ __device__ __forceinline__ void align16_body(const AlignArgs& A) {
   __shared__ uint32_t pref_all[Front16<NREG>::wpb][64];
   __shared__ int erec_all[Front16<NREG>::wpb][8];  // NEXT #4 end-score records
   constexpr bool kSplit = AGATHA_SPLIT16 && NREG == 16;
-  __shared__ __align__(16) uint32_t rows_all[kSplit ? Front16<NREG>::wpb : 1][kSplit ? 4 * 32 * kRowS : 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int unit = blockIdx.x * Front16<NREG>::wpb + warp, nunits = gridDim.x * Front16<NREG>::wpb;
   int k = 0;
@@ -2331,7 +2274,7 @@ __device__ __forceinline__ void align16_body(const AlignArgs& A) {
     q = __shfl_sync(kFull, q, 0);
     if ((uint32_t)q >= A.n_pairs) break;
     if constexpr (kSplit)
-      align_pair16s<NREG, TRACE, NCAP, ENDS>(A, A.order[q], lane, snap_all[warp], rows_all[warp], unit, erec_all[warp]);
+      align_pair16s<NREG, TRACE, NCAP, ENDS>(A, A.order[q], lane, snap_all[warp], unit, erec_all[warp]);
     else
       align_pair16<NREG, TRACE, NCAP, ENDS>(A, A.order[q], lane, snap_all[warp], pref_all[warp], unit, erec_all[warp]);
   }
