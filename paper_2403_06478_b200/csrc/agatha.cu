@@ -1877,6 +1877,11 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
     }
     const bool nmap = A.nmap != 0;
     int err = 0;
+    // every base of both sequences is validated (the streams below cover only the
+    // positions the band can reach, which for very unequal lengths is not all of them)
+    for (int x = lane; x < m; x += 32) base_code(ps.ref[r0 + x], nmap, &err);
+    for (int x = lane; x < n; x += 32) base_code(ps.qry[q0 + x], nmap, &err);
+    int err_unused = 0;
     uint32_t* BR = WR + L;  // byte codes | 0x80: BR[ix] for x = u0 + ix, BQ[iy] for y = ylo + iy
     uint32_t* BQ = VQ + L;
     const int NBW = (L + 264) / 4;
@@ -1888,11 +1893,11 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
       for (int t = 0; t < 4; ++t) {
         const int x = u0 + 4 * w + t;  // R position (1-based)
         uint32_t c = 8;
-        if (x >= 1 && x <= m) c = base_code(ref[x - 1], nmap, &err);
+        if (x >= 1 && x <= m) c = base_code(ref[x - 1], nmap, &err_unused);
         br4 |= (c | 0x80u) << (8 * t);
         const int y = ylo + 4 * w + t;  // reversed-Q position: Q_{n - y}
         c = 8;
-        if (y >= 0 && y < n) c = base_code(qry[n - 1 - y], nmap, &err);
+        if (y >= 0 && y < n) c = base_code(qry[n - 1 - y], nmap, &err_unused);
         bq4 |= (c | 0x80u) << (8 * t);
       }
       BR[w] = br4;

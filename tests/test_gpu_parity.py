@@ -419,6 +419,26 @@ def test_error_codes(gpu_lib, ctx):
     assert e.value.code == gpu_lib.ERANGE
 
 
+@pytest.mark.parametrize("w", [500, 200, 100])
+def test_bad_base_beyond_the_band(gpu_lib, ctx, kflags, w):
+    """A non-ACGTN byte is refused wherever it sits, also where the band never reaches
+    (very unequal lengths: R bases past n + w, Q bases past m + w), on every front; with
+    N_MAP it reads as N, exactly as in the oracle (R17)."""
+    rng = np.random.default_rng(5000 + w)
+    a = "".join("ACGT"[x] for x in rng.integers(0, 4, 20000))
+    b = "".join("ACGT"[x] for x in rng.integers(0, 4, 1200))
+    for R, Q in ((a[:19000] + "X" + a[19001:], b), (b, a[:19500] + "x" + a[19501:])):
+        pairs = synth.from_list([(R, Q), (a[:3000], a[5:3000])])
+        params = dict(SCORING, band_left=w, band_right=w, zdrop=-1)
+        with pytest.raises(gpu_lib.AgathaError) as e:
+            gpu_lib.align_pairs(ctx, pairs, params, flags=kflags)
+        assert e.value.code == gpu_lib.ECHAR
+        got = gpu_lib.align_pairs(ctx, pairs, params, flags=kflags | gpu_lib.N_MAP)
+        mapped = synth.from_list([(R.replace("X", "N"), Q.replace("x", "N")), (a[:3000], a[5:3000])])
+        rc, exp, _ = oracle.align_batch(mapped, params)
+        assert rc == 0 and got.tobytes() == exp.tobytes()
+
+
 def test_variant_golden_on_gpu(gpu_lib, ctx, kflags):
     from test_oracle import VARIANTS
     for R, Q, params, expected, cite in VARIANTS:
