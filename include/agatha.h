@@ -164,6 +164,8 @@ typedef struct {
   int32_t rebase_iters; /* 16-bit kernels: iterations between re-centrings of the 32-slot
                           front (128, 64 or 32, the longest the 16-bit guard admits), 0
                           when the 16-bit kernels do not apply                           */
+  int32_t pin_off8;    /* 16-slot front: the common low padding off = (-D) mod 8 of its pairs
+                          when its pinned instantiation ran, else -1                     */
 } agatha_stats_t;
 
 /* Create a context on CUDA device `cuda_device`.  Fails with AGATHA_ECUDA when the

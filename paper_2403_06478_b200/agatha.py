@@ -59,7 +59,7 @@ class Stats(ctypes.Structure):
                 ("packed16", ctypes.c_int32), ("warps_per_pair", ctypes.c_int32),
                 ("tier_pairs", ctypes.c_int32 * 3), ("input_chunks", ctypes.c_int32),
                 ("lpt_from_chunk", ctypes.c_int32), ("pin_off", ctypes.c_int32),
-                ("rebase_iters", ctypes.c_int32)]
+                ("rebase_iters", ctypes.c_int32), ("pin_off8", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: (list(v) if k == "tier_pairs" else v)

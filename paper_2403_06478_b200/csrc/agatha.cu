@@ -2345,7 +2345,7 @@ struct PrepArgs {
                                 // range): the queue reaches them after they have arrived
   int* tier_count;              // [3] pairs per slot tier (tier_of)
   int* max_off16_t0;            // max (-D) mod 16 over the pairs of tier 0
-  int* off_mask16;              // [2] OR of 1 << ((-D) mod 16) over the batch / its tier 0
+  int* off_mask16;              // OR of 1 << ((-D) mod 16) over: [0] the batch, [1] its tier 0, [8] its tier 1
   unsigned long long* len_hash; // shared queue (NEXT #1): sum over pairs of a hash of
                                 // (p, m, n), the batch part of the queue fingerprint
 };
@@ -2437,6 +2437,8 @@ __global__ void prep_kernel(PrepArgs P) {
           if (tier_of(D) == 0) {
             atomicMax(P.max_off16_t0, (int)((-D) & 15));
             if (P.off_mask16) atomicOr(P.off_mask16 + 1, 1 << ((-D) & 15));
+          } else if (tier_of(D) == 1 && P.off_mask16) {
+            atomicOr(P.off_mask16 + 8, 1 << ((-D) & 15));
           }
         }
       }
@@ -2663,6 +2665,21 @@ int launch_pin16(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid
   }
   return AGATHA_EINVAL;
 }
+template <int OFF>
+int launch_pin8(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int* units_out, bool dry,
+                int off) {
+  if constexpr (OFF < 8) {
+    if (off == OFF) return launch_align16<8, false, 100 + OFF>(ctx, A, st, grid_out, units_out, dry);
+    return launch_pin8<OFF + 1>(ctx, A, st, grid_out, units_out, dry, off);
+  }
+  return AGATHA_EINVAL;
+}
+// the 16-slot front: pinned (one capped slot) when the launch's pairs share their off
+inline int launch_align16_mid(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out,
+                              int* units_out, bool dry, int pin) {
+  if (AGATHA_PIN && pin >= 0) return launch_pin8<0>(ctx, A, st, grid_out, units_out, dry, pin);
+  return launch_align16<8, false, NCAP8>(ctx, A, st, grid_out, units_out, dry);
+}
 template <bool ENDS>
 int launch_align16_wide(agatha_ctx* ctx, const AlignArgs& A, cudaStream_t st, int* grid_out, int maxoff,
                         int* units_out = nullptr, bool dry = false, int pin = -1) {
@@ -2883,7 +2900,7 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   int launches = 1, lib_launches = 0;
   const uint32_t* d_order = (const uint32_t*)ctx->iota.p;
   // K (slots per lane) from the widest band in the batch
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 72, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_scalars, d_sc, 76, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   const int err0 = ctx->h_scalars[0], maxD = ctx->h_scalars[1], maxoff16 = ctx->h_scalars[3];
   const int tier_n[3] = {ctx->h_scalars[4], ctx->h_scalars[5], ctx->h_scalars[6]};
@@ -2894,6 +2911,12 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
   ctx->stats.pin_off = -1;
   ctx->stats.rebase_iters = iv16;
   const int pin_t0 = pin16_ok(p, iv16) ? pin_off(ctx->h_scalars[11]) : -1;
+  // the 16-slot front (paired layout, re-centring every kRebase16): its low padding is
+  // off = (-D) mod 8, common to a launch's pairs when their (-D) mod 16 agree mod 8
+  auto fold8 = [](int m16) { return (m16 | (m16 >> 8)) & 0xFF; };
+  const int pin8_all = (iv16 > 0 && pin16_ok(p, kRebase16)) ? pin_off(fold8(ctx->h_scalars[10])) : -1;
+  const int pin8_t1 = (iv16 > 0 && pin16_ok(p, kRebase16)) ? pin_off(fold8(ctx->h_scalars[18])) : -1;
+  ctx->stats.pin_off8 = -1;
   const int max_m = ctx->h_scalars[16], max_n = ctx->h_scalars[17];
   if (dev_in) {
     tot_r = h_tot[0];
@@ -3057,7 +3080,10 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
           rc = launch_align16_wide<false>(ctx, At, ts, &g, maxoff16_t0, &u, dry, pin_t0);
           ctx->stats.pin_off = AGATHA_PIN ? pin_t0 : -1;
         }
-        else if (t == 1) rc = launch_align16<8, false, NCAP8>(ctx, At, ts, &g, &u, dry);
+        else if (t == 1) {
+          rc = launch_align16_mid(ctx, At, ts, &g, &u, dry, pin8_t1);
+          ctx->stats.pin_off8 = AGATHA_PIN ? pin8_t1 : -1;
+        }
         else rc = launch_align16<4, false, 3>(ctx, At, ts, &g, &u, dry);
       }
       unit_base += u;
@@ -3080,7 +3106,11 @@ int run_batch(agatha_ctx* ctx, const agatha_batch_t* b, const agatha_params_t* p
       else if (t == 1) rc = launch_align16<8, false, NCAP8, true>(ctx, A, st, &grid, u, dry);
       else rc = launch_align16_wide<true>(ctx, A, st, &grid, maxoff16, u, dry);
     } else if (t == 2) rc = tr ? launch_align16<4, true, 3>(ctx, A, st, &grid, u, dry) : launch_align16<4, false, 3>(ctx, A, st, &grid, u, dry);
-    else if (t == 1) rc = tr ? launch_align16<8, true, NCAP8>(ctx, A, st, &grid, u, dry) : launch_align16<8, false, NCAP8>(ctx, A, st, &grid, u, dry);
+    else if (t == 1 && tr) rc = launch_align16<8, true, NCAP8>(ctx, A, st, &grid, u, dry);
+    else if (t == 1) {
+      rc = launch_align16_mid(ctx, A, st, &grid, u, dry, pin8_all);
+      ctx->stats.pin_off8 = AGATHA_PIN ? pin8_all : -1;
+    }
     else if (tr) rc = launch_align16<16, true, 16>(ctx, A, st, &grid, u, dry);
     else {
       rc = launch_align16_wide<false>(ctx, A, st, &grid, maxoff16, u, dry, pin_all);

@@ -131,6 +131,22 @@ def test_pinned_front_every_offset(gpu_lib, ctx, off):
         assert st["packed16"] == 1 and st["tier_pairs"][0] == pairs.n_pairs and st["pin_off"] == off, st
 
 
+@pytest.mark.parametrize("off", list(range(8)))
+def test_pinned_16slot_front_every_offset(gpu_lib, ctx, off):
+    """The 16-slot front's pinned instantiation (paired layout, one capped padding slot) at
+    every off = (-D) mod 8 with 256 < D <= 512: bit-exact with the oracle, with and without
+    Z-drop, and the stats name it."""
+    D = 512 - off
+    bl = (D - 1) // 2
+    br = D - 1 - bl
+    rng = np.random.default_rng(9300 + off)
+    pairs = synth.from_list(_pin_stress_pairs(rng, bl, br))
+    for z in (-1, 60):
+        compare(gpu_lib, ctx, pairs, dict(SCORING, band_left=bl, band_right=br, zdrop=z))
+        st = ctx.stats()
+        assert st["tier_pairs"][1] == pairs.n_pairs and st["pin_off8"] == off, st
+
+
 def test_pinned_front_fast_rising_padding(gpu_lib, ctx):
     """Scoring with about the largest S + 2 alpha the 16-bit guard admits at D = 1001 (23) under a
     band whose padding diagonals match everywhere (the dead slots' fastest rise): the
