@@ -949,7 +949,7 @@ __global__ void __launch_bounds__(32 * W, 12 / W) align_wide_kernel(AlignArgs A)
 //   STEADYC  the steady phase keeps the previous anti-diagonal's cell range and base
 //            instead of re-setting them every step (re-centring adjusts rH_prev)
 #ifndef AGATHA_LMTREE
-#define AGATHA_LMTREE 1
+#define AGATHA_LMTREE 0  // the split front: the serial lane max schedules better (4345 vs 4246 GCUPS)
 #endif
 #ifndef AGATHA_SNAP128
 #define AGATHA_SNAP128 0
