@@ -1790,6 +1790,12 @@ __device__ void align_pair16(const AlignArgs& A, uint32_t pid, int lane, uint32_
 #ifndef AGATHA_SPLIT16
 #define AGATHA_SPLIT16 1  // 0: the 32-slot front keeps the paired (j, j + NREG) layout
 #endif
+#ifndef AGATHA_SPLITLATE
+#define AGATHA_SPLITLATE 0  // split front: the window shift at the end of the iteration
+#endif
+#ifndef AGATHA_SPLITS2E
+#define AGATHA_SPLITS2E 0   // split front: both steps' score lookups at the top of the iteration
+#endif
 #ifndef AGATHA_STREAM_PF
 #define AGATHA_STREAM_PF 256  // split front: L2 prefetch distance of the stream loads (words), 0 = none
 #endif
@@ -2081,12 +2087,18 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
   };
   auto iteration = [&](auto masked_tag) {
     constexpr bool MASKED = decltype(masked_tag)::value;
-    uint32_t S2[NREG / 2], V2 = 0u;
+    uint32_t S2[NREG / 2], S2b[AGATHA_SPLITS2E ? NREG / 2 : 1], V2 = 0u;
     const int u = (cb + dls) >> 1;
     // ---- step PAR = 0, anti-diagonal cb ----
     {
 #pragma unroll
       for (int k = 0; k < NREG / 2; ++k) S2[k] = prmt(T0, T1, xs[k]);
+      if (AGATHA_SPLITS2E) {  // both steps' lookups up front; the next words right after
+#pragma unroll
+        for (int k = 0; k < NREG / 2; ++k) S2b[k] = prmt(T0, T1, hi_to_lo(xs[k], k65536));
+        shift_win(itc + 1);
+        load_xs();
+      }
       int tlo = 0, thi = HV + LC - 1;
       if (MASKED) {
         const int ib = u + lane * LC, jb = u - dls - lane * LC;
@@ -2108,10 +2120,17 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
     }
     // ---- step PAR = 1, anti-diagonal cb + 1 ----
     {
+      if (AGATHA_SPLITS2E) {
 #pragma unroll
-      for (int k = 0; k < NREG / 2; ++k) S2[k] = prmt(T0, T1, hi_to_lo(xs[k], k65536));
-      shift_win(itc + 1);
-      load_xs();
+        for (int k = 0; k < NREG / 2; ++k) S2[k] = S2b[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < NREG / 2; ++k) S2[k] = prmt(T0, T1, hi_to_lo(xs[k], k65536));
+      }
+      if (!AGATHA_SPLITLATE && !AGATHA_SPLITS2E) {
+        shift_win(itc + 1);
+        load_xs();
+      }
       int tlo = 0, thi = HV + LC - 1;
       if (MASKED) {
         const int ib = u + 1 + lane * LC, jb = u - dls - lane * LC;
@@ -2129,6 +2148,10 @@ __device__ void align_pair16s(const AlignArgs& A, uint32_t pid, int lane, uint32
         B_prev = s.B;
         tlo_prev = MASKED ? tlo : 0;
         thi_prev = MASKED ? thi : HV + LC - 1;
+      }
+      if (AGATHA_SPLITLATE && !AGATHA_SPLITS2E) {
+        shift_win(itc + 1);
+        load_xs();
       }
     }
     cb += 2;
