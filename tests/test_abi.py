@@ -66,3 +66,27 @@ def test_no_device_fails_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(agatha.AgathaError):
         agatha.Context(0)
+
+
+def test_binding_structs_match_the_header(tmp_path):
+    """The ctypes mirrors of the ABI structs have the header's size and field offsets (the
+    stats struct grew this round; a stale mirror would read the wrong fields)."""
+    import ctypes
+
+    from paper_2403_06478_b200 import agatha
+    pairs = {"agatha_params_t": agatha.Params, "agatha_batch_t": agatha.Batch, "agatha_stats_t": agatha.Stats}
+    src = tmp_path / "sizes.c"
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "agatha.h"', "int main(void) {"]
+    for cname, py in pairs.items():
+        lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "sizes"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split("\n") if l)
+    for cname, py in pairs.items():
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)
